@@ -1,0 +1,152 @@
+/*
+ * pmrc.h — C ABI of libpmrc: B200-native (sm_100a) product-matrix regenerating codes
+ * (Rashmi et al. MSR/MBR) made fast as in arxiv 1412.3022, "Fast Product-Matrix Regenerating
+ * Codes" (Le Scouarnec).  Citations: P:L = PAPER.md line L, S:L = SPEC.md line L; readings R1..R14
+ * are listed in DESIGN.md §3.
+ *
+ * Field: GF(2^8), primitive polynomial 0x11D, g = 2 (R1).  Symbols are bytes; a "block"
+ * (the paper's block) is S bytes; a "stripe" is one codeword: B data blocks encoded
+ * into n*alpha blocks, alpha per node.  Node ids are 0-based here (the paper is
+ * 1-based): nodes 0..k-1 are systematic, k..n-1 parity.
+ *
+ * Memory layouts (all buffers are caller-owned DEVICE memory on the device the code was created
+ * on, except pmrc_encode_host which takes pinned or pageable HOST memory):
+ *   data    [stripes][B][S]            block c of stripe t at data + t*B*S + c*S
+ *   parity  [stripes][(n-k)*alpha][S]  parity node p (p >= k), symbol j at
+ *                                       parity + t*P*S + ((p-k)*alpha + j)*S,  P = (n-k)*alpha
+ *   piece   a node's alpha blocks of one stripe, contiguous: [alpha][S]; a pmrc_region gives
+ *           the piece of stripe 0 (ptr) and the distance between consecutive stripes' pieces.
+ *   For MSR/RS, systematic node i's piece is the data view data + t*B*S + i*alpha*S
+ *   (stripe_stride B*S); parity node p's piece is the parity view above (stripe_stride P*S).
+ *   For MBR (R6), systematic node i stores row i of the message matrix M(X): symbol j
+ *   is data block L_{i,j}; such pieces must be materialised by the caller (pmrc_layout gives L).
+ *
+ * Alignment (GPU-path restriction, not the paper's): S % 16 == 0, every block address 16-byte
+ * aligned (ptr and stripe_stride multiples of 16).  Violations return PMRC_EALIGN.
+ *
+ * All data-path calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default
+ * stream) and never synchronise.  They return synchronously-detected errors only; faults of
+ * earlier launches surface as PMRC_ECUDA on a later call.  A handle may be used from one host
+ * thread at a time.
+ */
+#ifndef PMRC_H
+#define PMRC_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pmrc_code pmrc_code;
+
+/* code kinds */
+enum {
+  PMRC_MSR_SPARSE = 0,       /* the paper's sparse MSR: Phi = [I; Cauchy], Lambda Moebius */
+  PMRC_MSR_VANILLA = 1,      /* Rashmi et al. Vandermonde MSR */
+  PMRC_MBR = 2,              /* systematic MBR, Psi = [I_k 0; Cauchy] (R5) */
+  PMRC_RS_VANDERMONDE = 3    /* systematic Vandermonde Reed-Solomon baseline (R12); d = k */
+};
+
+/* error codes */
+enum {
+  PMRC_OK = 0,
+  PMRC_EINVAL = -1,       /* null pointer, id out of range / duplicated, wrong counts */
+  PMRC_EUNSUPPORTED = -2, /* w != 8; MSR with d != 2k-2; field too small; invalid construction */
+  PMRC_ESINGULAR = -3,    /* survivors do not span the data / helper matrix Psi_H singular (R10) */
+  PMRC_EALIGN = -4,       /* S % 16 != 0 or a block address not 16-byte aligned */
+  PMRC_ENOMEM = -5,       /* host or device allocation failed */
+  PMRC_ECUDA = -6,        /* CUDA runtime / driver error (details in pmrc_last_error) */
+  PMRC_EJIT = -7          /* kernel generation or NVRTC compilation failed */
+};
+
+/* A node piece region: piece of stripe t starts at ptr + t*stripe_stride (bytes). */
+typedef struct {
+  const void *ptr;
+  size_t stripe_stride;
+} pmrc_cregion;
+typedef struct {
+  void *ptr;
+  size_t stripe_stride;
+} pmrc_region;
+
+typedef struct {
+  int kind, n, k, d, w;
+  int alpha;           /* blocks per node */
+  int B;               /* data blocks per stripe, k*Delta */
+  int parity_rows;     /* (n-k)*alpha: rows of G'' */
+  int nnz;             /* nonzeros of G'' (the multiply-XORs per byte position) */
+  double zero_pct;     /* 100 * zeros / size of G'' (Table 1) */
+  int repair_complete; /* 1 if every d-subset of rows of Psi is invertible, so every
+                          (lost, helpers) repair succeeds; 0 for sparse MSR at n >= 2k (R10) */
+  long xor_ops;        /* LOP3 lane-ops per 32 byte positions of the encode XOR program
+                          (after common-subexpression elimination), 0 before generation */
+  long xor_ops_naive;  /* the naive bit-matrix count W of SURVEY §8(d) (roofline term) */
+} pmrc_info_t;
+
+/* Build the code: Psi, L, G, G' = G Gtilde^{-1}, G''; generate and compile the encode
+ * kernel for the CUDA device current at the call (the paper's "initialization").
+ * w must be 8.  For RS d is ignored (taken = k).  *out receives a handle to free with
+ * pmrc_destroy. */
+int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w);
+void pmrc_destroy(pmrc_code *c);
+int pmrc_info(const pmrc_code *c, pmrc_info_t *out);
+
+/* Copy matrices out (host memory).  which: 0 = Psi (n x d; RS n x k), 1 = G (n alpha x B),
+ * 2 = G' (n alpha x B), 3 = G'' (parity_rows x B), 4 = lambda (n).  rows/cols receive the shape;
+ * buf may be NULL to query the shape; otherwise it must hold rows*cols bytes. */
+int pmrc_matrix(const pmrc_code *c, int which, uint8_t *buf, int *rows, int *cols);
+/* Index matrix L, 1-based data indices, 0 = structural zero: MSR d x alpha, MBR d x d,
+ * RS: k x 1 (identity layout).  buf may be NULL to query the shape. */
+int pmrc_layout(const pmrc_code *c, int *buf, int *rows, int *cols);
+
+/* Systematic encode: parity = G'' data for `stripes` stripes of B blocks of S bytes.
+ * Zero coefficients are skipped at kernel-generation time. */
+int pmrc_encode(pmrc_code *c, const void *data, void *parity, size_t S, size_t stripes, void *stream);
+
+/* Same computation from HOST buffers (pinned memory recommended): the library stages chunks of
+ * stripes through device buffers it owns (2 x chunk), overlapping H2D, the encode kernel and D2H
+ * on `stream` plus an internal copy stream.  Synchronises before returning. */
+int pmrc_encode_host(pmrc_code *c, const void *data_host, void *parity_host, size_t S, size_t stripes,
+                     void *stream);
+
+/* Lazy linear decode: given n_surv >= k surviving node ids and their pieces,
+ * write the data blocks that are NOT held by a surviving systematic node into data_out
+ * ([stripes][B][S]; other blocks are left untouched, so passing the data buffer itself completes
+ * it in place).  Rows of G' are chosen systematic-first, then ascending id (R13); the B x B
+ * inversion is done once per survivor set and cached.  *n_written (may be NULL) receives
+ * the number of data blocks written per stripe.  PMRC_ESINGULAR if the survivors do not span B. */
+int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregion *pieces, void *data_out,
+                size_t S, size_t stripes, int *n_written, void *stream);
+
+/* Exact repair of node lost_id from d helpers (RS: k), P:53 footnote: helper h
+ * contributes beta_h = mu . piece_h (mu = phi_f for MSR, psi_f for MBR; only blocks with nonzero
+ * mu are read); the newcomer solves Psi_H z = beta (cached d x d inversion) and forms its
+ * alpha blocks (MSR: z_a + lambda_f z_{alpha+a}; MBR: z).  One fused launch.  out_piece receives
+ * the lost node's piece.  PMRC_ESINGULAR when Psi_H is singular (R10). */
+int pmrc_repair(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers, const pmrc_cregion *helper_pieces,
+                pmrc_region out_piece, size_t S, size_t stripes, void *stream);
+
+/* The two halves of repair as separate calls (the helper side and the newcomer side, which in a
+ * storage system run on different machines):  beta (one block per stripe) = mu . piece. */
+int pmrc_repair_project(pmrc_code *c, int lost_id, pmrc_cregion piece, pmrc_region beta, size_t S, size_t stripes,
+                        void *stream);
+/* newcomer: out_piece from the d helpers' betas (betas[i] belongs to helper_ids[i]). */
+int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers, const pmrc_cregion *betas,
+                        pmrc_region out_piece, size_t S, size_t stripes, void *stream);
+
+/* Blocks each helper reads to repair lost_id: nnz(phi_f) (MSR: 1 if f < alpha else alpha,
+ * P:209), nnz(psi_f) for MBR, 1 for RS. */
+int pmrc_read_cost(const pmrc_code *c, int lost_id, int *blocks_per_helper);
+
+/* Number of kernels this library launched since load (for the bench's gpu_launches claim). */
+unsigned long long pmrc_launch_count(void);
+
+const char *pmrc_strerror(int err);
+/* Thread-local detail string of the last error raised on this thread. */
+const char *pmrc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMRC_H */

@@ -1,0 +1,189 @@
+"""Python binding of libpmrc (include/pmrc.h) — argument marshalling only.
+
+Every function below has the name of the C-ABI entry point it calls; buffers are passed as
+integer device addresses (e.g. ``tensor.data_ptr()``) and streams as ``cudaStream_t`` handles
+(e.g. ``torch.cuda.current_stream().cuda_stream``).  There is no CPU fallback: every data-path
+call runs the library's CUDA kernels and raises ``PmrcError`` on any error, including a missing
+GPU or a missing ``libpmrc.so``.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpmrc.so")
+
+PMRC_MSR_SPARSE, PMRC_MSR_VANILLA, PMRC_MBR, PMRC_RS_VANDERMONDE = 0, 1, 2, 3
+PMRC_OK, PMRC_EINVAL, PMRC_EUNSUPPORTED, PMRC_ESINGULAR = 0, -1, -2, -3
+PMRC_EALIGN, PMRC_ENOMEM, PMRC_ECUDA, PMRC_EJIT = -4, -5, -6, -7
+
+MATRIX_PSI, MATRIX_G, MATRIX_GSYS, MATRIX_GPP, MATRIX_LAMBDA = 0, 1, 2, 3, 4
+
+EXPORTS = ["pmrc_create", "pmrc_destroy", "pmrc_info", "pmrc_matrix", "pmrc_layout", "pmrc_encode",
+           "pmrc_encode_host", "pmrc_decode", "pmrc_repair", "pmrc_repair_project", "pmrc_repair_combine",
+           "pmrc_read_cost", "pmrc_launch_count", "pmrc_strerror", "pmrc_last_error"]
+
+
+class PmrcError(RuntimeError):
+    def __init__(self, rc, where, detail=""):
+        self.rc = rc
+        super().__init__("%s: %s (%d)%s" % (where, _strerror(rc), rc, (": " + detail) if detail else ""))
+
+
+class pmrc_cregion(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("stripe_stride", ctypes.c_size_t)]
+
+
+class pmrc_region(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("stripe_stride", ctypes.c_size_t)]
+
+
+class pmrc_info_t(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("n", ctypes.c_int), ("k", ctypes.c_int), ("d", ctypes.c_int),
+                ("w", ctypes.c_int), ("alpha", ctypes.c_int), ("B", ctypes.c_int), ("parity_rows", ctypes.c_int),
+                ("nnz", ctypes.c_int), ("zero_pct", ctypes.c_double), ("repair_complete", ctypes.c_int),
+                ("xor_ops", ctypes.c_long), ("xor_ops_naive", ctypes.c_long)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_L = None
+
+
+def lib():
+    """Load libpmrc.so (raises if it was not built: no fallback)."""
+    global _L
+    if _L is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError("libpmrc.so not built (run __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I, Z = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+        IP = ctypes.POINTER(ctypes.c_int)
+        sig = {
+            "pmrc_create": ([ctypes.POINTER(ctypes.c_void_p), I, I, I, I, I], I),
+            "pmrc_destroy": ([P], None),
+            "pmrc_info": ([P, ctypes.POINTER(pmrc_info_t)], I),
+            "pmrc_matrix": ([P, I, P, IP, IP], I),
+            "pmrc_layout": ([P, P, IP, IP], I),
+            "pmrc_encode": ([P, P, P, Z, Z, P], I),
+            "pmrc_encode_host": ([P, P, P, Z, Z, P], I),
+            "pmrc_decode": ([P, IP, I, ctypes.POINTER(pmrc_cregion), P, Z, Z, IP, P], I),
+            "pmrc_repair": ([P, I, IP, I, ctypes.POINTER(pmrc_cregion), pmrc_region, Z, Z, P], I),
+            "pmrc_repair_project": ([P, I, pmrc_cregion, pmrc_region, Z, Z, P], I),
+            "pmrc_repair_combine": ([P, I, IP, I, ctypes.POINTER(pmrc_cregion), pmrc_region, Z, Z, P], I),
+            "pmrc_read_cost": ([P, I, IP], I),
+            "pmrc_launch_count": ([], ctypes.c_ulonglong),
+            "pmrc_strerror": ([I], ctypes.c_char_p),
+            "pmrc_last_error": ([], ctypes.c_char_p),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _L = L
+    return _L
+
+
+def _strerror(rc):
+    try:
+        return lib().pmrc_strerror(rc).decode()
+    except Exception:
+        return "error"
+
+
+def _check(rc, where):
+    if rc != PMRC_OK:
+        raise PmrcError(rc, where, lib().pmrc_last_error().decode())
+
+
+def _ints(seq):
+    seq = [int(x) for x in seq]
+    return (ctypes.c_int * max(1, len(seq)))(*seq), len(seq)
+
+
+# ------------------------------------------------------------------ C-ABI mirrors
+def pmrc_create(kind, k, d, n, w=8):
+    h = ctypes.c_void_p()
+    _check(lib().pmrc_create(ctypes.byref(h), kind, k, d, n, w), "pmrc_create")
+    return h
+
+
+def pmrc_destroy(code):
+    lib().pmrc_destroy(code)
+
+
+def pmrc_info(code):
+    info = pmrc_info_t()
+    _check(lib().pmrc_info(code, ctypes.byref(info)), "pmrc_info")
+    return info.as_dict()
+
+
+def pmrc_matrix(code, which):
+    import numpy as np
+    r, c = ctypes.c_int(), ctypes.c_int()
+    _check(lib().pmrc_matrix(code, which, None, ctypes.byref(r), ctypes.byref(c)), "pmrc_matrix")
+    out = np.zeros((r.value, c.value), np.uint8)
+    _check(lib().pmrc_matrix(code, which, out.ctypes.data, ctypes.byref(r), ctypes.byref(c)), "pmrc_matrix")
+    return out
+
+
+def pmrc_layout(code):
+    import numpy as np
+    r, c = ctypes.c_int(), ctypes.c_int()
+    _check(lib().pmrc_layout(code, None, ctypes.byref(r), ctypes.byref(c)), "pmrc_layout")
+    out = np.zeros((r.value, c.value), np.int32)
+    _check(lib().pmrc_layout(code, out.ctypes.data, ctypes.byref(r), ctypes.byref(c)), "pmrc_layout")
+    return out
+
+
+def pmrc_encode(code, data_ptr, parity_ptr, S, stripes, stream=0):
+    _check(lib().pmrc_encode(code, data_ptr, parity_ptr, S, stripes, stream), "pmrc_encode")
+
+
+def pmrc_encode_host(code, data_host_ptr, parity_host_ptr, S, stripes, stream=0):
+    _check(lib().pmrc_encode_host(code, data_host_ptr, parity_host_ptr, S, stripes, stream), "pmrc_encode_host")
+
+
+def pmrc_decode(code, surv_ids, pieces, data_out_ptr, S, stripes, stream=0):
+    """pieces: list of (ptr, stripe_stride) per survivor.  Returns blocks written per stripe."""
+    ids, n = _ints(surv_ids)
+    regs = (pmrc_cregion * max(1, n))(*[pmrc_cregion(p, s) for p, s in pieces])
+    nw = ctypes.c_int()
+    _check(lib().pmrc_decode(code, ids, n, regs, data_out_ptr, S, stripes, ctypes.byref(nw), stream), "pmrc_decode")
+    return nw.value
+
+
+def pmrc_repair(code, lost_id, helper_ids, helper_pieces, out_piece, S, stripes, stream=0):
+    ids, n = _ints(helper_ids)
+    regs = (pmrc_cregion * max(1, n))(*[pmrc_cregion(p, s) for p, s in helper_pieces])
+    _check(lib().pmrc_repair(code, lost_id, ids, n, regs, pmrc_region(*out_piece), S, stripes, stream), "pmrc_repair")
+
+
+def pmrc_repair_project(code, lost_id, piece, beta, S, stripes, stream=0):
+    _check(lib().pmrc_repair_project(code, lost_id, pmrc_cregion(*piece), pmrc_region(*beta), S, stripes, stream),
+           "pmrc_repair_project")
+
+
+def pmrc_repair_combine(code, lost_id, helper_ids, betas, out_piece, S, stripes, stream=0):
+    ids, n = _ints(helper_ids)
+    regs = (pmrc_cregion * max(1, n))(*[pmrc_cregion(p, s) for p, s in betas])
+    _check(lib().pmrc_repair_combine(code, lost_id, ids, n, regs, pmrc_region(*out_piece), S, stripes, stream),
+           "pmrc_repair_combine")
+
+
+def pmrc_read_cost(code, lost_id):
+    b = ctypes.c_int()
+    _check(lib().pmrc_read_cost(code, lost_id, ctypes.byref(b)), "pmrc_read_cost")
+    return b.value
+
+
+def pmrc_launch_count():
+    return int(lib().pmrc_launch_count())
+
+
+def pmrc_strerror(rc):
+    return _strerror(rc)
+
+
+def pmrc_last_error():
+    return lib().pmrc_last_error().decode()

@@ -1,0 +1,63 @@
+"""In-tree build of libpmrc.so (host C++ + NVRTC JIT) and the shared input generator.
+
+The bitsliced kernels are generated per plan and compiled by NVRTC for sm_100a at
+``pmrc_create`` / first use (``-arch=sm_100a``); ``build()`` also nvcc-compiles the generated
+encode kernels of the benchmark configurations for sm_100a as a compile check and SASS artefact.
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+HOST_SRC = ["gf256.cpp", "construct.cpp", "xorprog.cpp", "plan.cpp", "cudrv.cpp", "capi.cpp"]
+LIB = os.path.join(HERE, "libpmrc.so")
+INPUTS_LIB = os.path.join(ROOT, "inputs", "libpmrc_inputs.so")
+NVCC_ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError("build failed: %s" % cmd[0])
+    return r
+
+
+def _stale(target, sources):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def build_lib(force=False):
+    srcs = [os.path.join(HERE, "csrc", "host", s) for s in HOST_SRC]
+    deps = srcs + [os.path.join(HERE, "csrc", "host", h) for h in os.listdir(os.path.join(HERE, "csrc", "host"))
+                   if h.endswith(".hpp")] + [os.path.join(ROOT, "include", "pmrc.h")]
+    if force or _stale(LIB, deps):
+        _run(["g++", "-O2", "-g", "-std=c++17", "-fPIC", "-shared", "-Wall", "-Wno-unused-function",
+              "-I" + os.path.join(CUDA, "include"), "-o", LIB] + srcs +
+             ["-L" + os.path.join(CUDA, "lib64"), "-lnvrtc", "-lcudart", "-ldl", "-lpthread",
+              "-Wl,-rpath," + os.path.join(CUDA, "lib64")])
+    return LIB
+
+
+def build_inputs(force=False):
+    src = os.path.join(ROOT, "inputs", "pmrc_inputs.cu")
+    hdr = os.path.join(ROOT, "inputs", "pmrc_inputs.h")
+    if force or _stale(INPUTS_LIB, [src, hdr]):
+        _run([os.path.join(CUDA, "bin", "nvcc")] + NVCC_ARCH +
+             ["-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "-o", INPUTS_LIB, src])
+    return INPUTS_LIB
+
+
+def build_all(force=False):
+    build_inputs(force)
+    build_lib(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)
+    print("built", LIB, INPUTS_LIB)

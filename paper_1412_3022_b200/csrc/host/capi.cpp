@@ -1,0 +1,612 @@
+// C ABI of libpmrc (include/pmrc.h): code handles, plan caches, and the data-path entry points.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../../include/pmrc.h"
+#include "construct.hpp"
+#include "plan.hpp"
+
+using namespace pmrc;
+
+namespace {
+thread_local std::string g_last_error;
+
+int fail(int rc, const std::string &msg) {
+  g_last_error = msg;
+  return rc;
+}
+
+struct HostStage {
+  size_t chunk_stripes = 0;
+  void *d_data[2] = {nullptr, nullptr};
+  void *d_par[2] = {nullptr, nullptr};
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr;
+  size_t bytes = 0;
+};
+}  // namespace
+
+struct pmrc_code {
+  CodeDef def;
+  int device = -1;
+  GenOptions gen;
+  PlanSpec enc_spec;
+  Kernel enc;
+  bool enc_built = false;
+  GenStats enc_stats;
+  std::map<std::string, std::unique_ptr<Kernel>> plans;  // decode / repair / project / combine
+  std::map<std::string, int> plan_err;                   // cached failures (ESINGULAR)
+  std::map<std::string, int> plan_meta;                  // e.g. blocks written by a decode plan
+  HostStage hs;
+};
+
+namespace {
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+int check_region(const void *p, size_t stride, size_t stripes) {
+  if (!p) return PMRC_EINVAL;
+  if (!aligned16(p) || (stripes > 1 && (stride & 15))) return PMRC_EALIGN;
+  return PMRC_OK;
+}
+
+int ensure_device(pmrc_code *c) {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(PMRC_ECUDA, "no CUDA device available (the GPU path has no CPU fallback)");
+  }
+  if (c->device < 0) c->device = dev;
+  if (dev != c->device) return fail(PMRC_EINVAL, "handle was created for another CUDA device");
+  return PMRC_OK;
+}
+
+int get_kernel(pmrc_code *c, const std::string &key, const PlanSpec &spec, Kernel **out) {
+  auto it = c->plans.find(key);
+  if (it != c->plans.end()) {
+    *out = it->second.get();
+    return PMRC_OK;
+  }
+  int rc = ensure_device(c);
+  if (rc) return rc;
+  auto k = std::make_unique<Kernel>();
+  std::string err;
+  rc = build_kernel(spec, c->gen, *k, err);
+  if (rc) return fail(rc, err);
+  *out = k.get();
+  c->plans[key] = std::move(k);
+  return PMRC_OK;
+}
+
+int build_encode(pmrc_code *c) {
+  if (c->enc_built) return PMRC_OK;
+  int rc = ensure_device(c);
+  if (rc) return rc;
+  std::string err;
+  rc = build_kernel(c->enc_spec, c->gen, c->enc, err);
+  if (rc) return fail(rc, err);
+  c->enc_built = true;
+  return PMRC_OK;
+}
+
+std::string ids_key(const char *tag, const int *ids, int n, int extra) {
+  std::string k = tag;
+  k += ":" + std::to_string(extra);
+  for (int i = 0; i < n; i++) k += "," + std::to_string(ids[i]);
+  return k;
+}
+
+int check_ids(const CodeDef &d, const int *ids, int n) {
+  for (int i = 0; i < n; i++) {
+    if (ids[i] < 0 || ids[i] >= d.n) return PMRC_EINVAL;
+    for (int j = 0; j < i; j++)
+      if (ids[i] == ids[j]) return PMRC_EINVAL;
+  }
+  return PMRC_OK;
+}
+
+// repair coefficient vector mu of lost node f (MSR: phi_f; MBR: psi_f; RS: [1])
+std::vector<uint8_t> repair_mu(const CodeDef &d, int f) {
+  if (d.kind == KIND_RS) return {1};
+  int m = (d.kind == KIND_MBR) ? d.d : d.alpha;
+  std::vector<uint8_t> mu(m);
+  for (int t = 0; t < m; t++) mu[t] = d.psi.at(f, t);
+  return mu;
+}
+
+// newcomer matrix R: out_a = sum_h R[a][h] beta_h  (alpha x n_helpers).  false if singular.
+bool repair_matrix(const CodeDef &d, int f, const int *H, Mat &R) {
+  if (d.kind == KIND_RS) {
+    // lost = G'_f (G'_H)^{-1} [c_h]
+    Mat GH(d.k, d.k), GHi;
+    for (int a = 0; a < d.k; a++)
+      for (int j = 0; j < d.k; j++) GH.at(a, j) = d.Gsys.at(H[a], j);
+    if (!invert(GH, GHi)) return false;
+    Mat row(1, d.k);
+    for (int j = 0; j < d.k; j++) row.at(0, j) = d.Gsys.at(f, j);
+    R = matmul(row, GHi);
+    return true;
+  }
+  Mat PH(d.d, d.d), PHi;
+  for (int a = 0; a < d.d; a++)
+    for (int j = 0; j < d.d; j++) PH.at(a, j) = d.psi.at(H[a], j);
+  if (!invert(PH, PHi)) return false;  // R10: predicted singular sets at n >= 2k
+  if (d.kind == KIND_MBR) {
+    R = PHi;  // piece = z = Psi_H^{-1} beta (M symmetric)
+    return true;
+  }
+  // MSR: piece_a = z_a + lambda_f z_{alpha+a}
+  Mat sel(d.alpha, d.d);
+  for (int a = 0; a < d.alpha; a++) {
+    sel.at(a, a) = 1;
+    sel.at(a, d.alpha + a) = d.lambda[f];
+  }
+  R = matmul(sel, PHi);
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *pmrc_strerror(int err) {
+  switch (err) {
+    case PMRC_OK: return "ok";
+    case PMRC_EINVAL: return "invalid argument";
+    case PMRC_EUNSUPPORTED: return "unsupported parameters";
+    case PMRC_ESINGULAR: return "singular (not decodable / repairable from this set)";
+    case PMRC_EALIGN: return "misaligned buffer or block size (GPU path needs S % 16 == 0, 16-B aligned blocks)";
+    case PMRC_ENOMEM: return "out of memory";
+    case PMRC_ECUDA: return "CUDA error";
+    case PMRC_EJIT: return "kernel generation / NVRTC compilation failed";
+    default: return "unknown error";
+  }
+}
+
+const char *pmrc_last_error(void) { return g_last_error.c_str(); }
+
+unsigned long long pmrc_launch_count(void) { return launch_counter(); }
+
+int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
+  if (!out) return fail(PMRC_EINVAL, "out is NULL");
+  *out = nullptr;
+  std::unique_ptr<pmrc_code> c(new (std::nothrow) pmrc_code());
+  if (!c) return fail(PMRC_ENOMEM, "host allocation");
+  std::string err;
+  if (kind == KIND_RS) d = k;
+  int rc = build_code(kind, k, d, n, w, c->def, err);
+  if (rc) return fail(rc, err);
+  // encode plan: inputs = data blocks (slot 0), outputs = parity rows (slot 1), A = G''
+  const CodeDef &D = c->def;
+  c->enc_spec.n_slots = 2;
+  for (int i = 0; i < D.B; i++) c->enc_spec.inputs.push_back({{{0, i, 1}}});
+  for (int r = 0; r < D.P; r++) c->enc_spec.outputs.push_back({1, r});
+  c->enc_spec.A = D.Gpp;
+  (void)generate_source(c->enc_spec, c->gen, c->enc_stats);  // XOR-program statistics
+  // compile now if a device is present (the paper's initialization); else on first use
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) {
+    rc = build_encode(c.get());
+    if (rc) return rc;
+  } else {
+    cudaGetLastError();
+  }
+  *out = c.release();
+  return PMRC_OK;
+}
+
+void pmrc_destroy(pmrc_code *c) {
+  if (!c) return;
+  int cur = -1;
+  bool have = cudaGetDevice(&cur) == cudaSuccess;
+  if (c->device >= 0 && have) cudaSetDevice(c->device);
+  free_kernel(c->enc);
+  for (auto &kv : c->plans) free_kernel(*kv.second);
+  for (int i = 0; i < 2; i++) {
+    if (c->hs.d_data[i]) cudaFree(c->hs.d_data[i]);
+    if (c->hs.d_par[i]) cudaFree(c->hs.d_par[i]);
+    if (c->hs.st[i]) cudaStreamDestroy(c->hs.st[i]);
+  }
+  if (c->hs.ev_start) cudaEventDestroy(c->hs.ev_start);
+  if (have && cur >= 0) cudaSetDevice(cur);
+  cudaGetLastError();
+  delete c;
+}
+
+int pmrc_info(const pmrc_code *c, pmrc_info_t *o) {
+  if (!c || !o) return fail(PMRC_EINVAL, "NULL argument");
+  const CodeDef &D = c->def;
+  memset(o, 0, sizeof(*o));
+  o->kind = D.kind; o->n = D.n; o->k = D.k; o->d = D.d; o->w = 8;
+  o->alpha = D.alpha; o->B = D.B; o->parity_rows = D.P;
+  long nnz = 0;
+  for (uint8_t v : D.Gpp.a) nnz += v != 0;
+  o->nnz = (int)nnz;
+  o->zero_pct = D.Gpp.a.empty() ? 0.0 : 100.0 * (double)(D.Gpp.a.size() - nnz) / (double)D.Gpp.a.size();
+  o->repair_complete = D.repair_complete ? 1 : 0;
+  o->xor_ops = c->enc_stats.xor2;
+  o->xor_ops_naive = c->enc_stats.naive_lop3;
+  return PMRC_OK;
+}
+
+int pmrc_matrix(const pmrc_code *c, int which, uint8_t *buf, int *rows, int *cols) {
+  if (!c || !rows || !cols) return fail(PMRC_EINVAL, "NULL argument");
+  const CodeDef &D = c->def;
+  const Mat *M = nullptr;
+  Mat lam;
+  switch (which) {
+    case 0: M = &D.psi; break;
+    case 1: M = &D.G; break;
+    case 2: M = &D.Gsys; break;
+    case 3: M = &D.Gpp; break;
+    case 4:
+      lam = Mat(1, D.n);
+      for (int i = 0; i < D.n && i < (int)D.lambda.size(); i++) lam.at(0, i) = D.lambda[i];
+      M = &lam;
+      break;
+    default: return fail(PMRC_EINVAL, "unknown matrix id");
+  }
+  *rows = M->r;
+  *cols = M->c;
+  if (buf) memcpy(buf, M->a.data(), M->a.size());
+  return PMRC_OK;
+}
+
+int pmrc_layout(const pmrc_code *c, int *buf, int *rows, int *cols) {
+  if (!c || !rows || !cols) return fail(PMRC_EINVAL, "NULL argument");
+  *rows = c->def.Lrows;
+  *cols = c->def.Lcols;
+  if (buf) memcpy(buf, c->def.Lidx.data(), sizeof(int) * c->def.Lidx.size());
+  return PMRC_OK;
+}
+
+int pmrc_encode(pmrc_code *c, const void *data, void *parity, size_t S, size_t stripes, void *stream) {
+  if (!c) return fail(PMRC_EINVAL, "NULL handle");
+  if (S == 0 || stripes == 0) return PMRC_OK;
+  if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
+  const CodeDef &D = c->def;
+  int rc = check_region(data, (size_t)D.B * S, stripes);
+  if (!rc) rc = check_region(parity, (size_t)D.P * S, stripes);
+  if (rc) return fail(rc, "bad data/parity pointer");
+  rc = build_encode(c);
+  if (rc) return rc;
+  uint64_t ptrs[2] = {(uint64_t)(uintptr_t)data, (uint64_t)(uintptr_t)parity};
+  uint64_t strides[2] = {(uint64_t)D.B * S, (uint64_t)D.P * S};
+  std::string err;
+  rc = launch_kernel(c->enc, ptrs, strides, S, stripes, stream, err);
+  if (rc) return fail(rc, err);
+  return PMRC_OK;
+}
+
+int pmrc_encode_host(pmrc_code *c, const void *data_host, void *parity_host, size_t S, size_t stripes, void *stream) {
+  if (!c || !data_host || !parity_host) return fail(PMRC_EINVAL, "NULL argument");
+  if (S == 0 || stripes == 0) return PMRC_OK;
+  if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
+  int rc = build_encode(c);
+  if (rc) return rc;
+  const CodeDef &D = c->def;
+  HostStage &h = c->hs;
+  const size_t in_b = (size_t)D.B * S, out_b = (size_t)D.P * S;
+  // chunks of ~64 MiB of source data, double buffered
+  size_t chunk = std::max<size_t>(1, ((size_t)64 << 20) / in_b);
+  chunk = std::min(chunk, stripes);
+  if (h.chunk_stripes < chunk) {
+    for (int i = 0; i < 2; i++) {
+      if (h.d_data[i]) cudaFree(h.d_data[i]);
+      if (h.d_par[i]) cudaFree(h.d_par[i]);
+      h.d_data[i] = h.d_par[i] = nullptr;
+      if (cudaMalloc(&h.d_data[i], chunk * in_b) != cudaSuccess || cudaMalloc(&h.d_par[i], chunk * out_b) != cudaSuccess) {
+        cudaGetLastError();
+        h.chunk_stripes = 0;
+        return fail(PMRC_ENOMEM, "staging buffers");
+      }
+    }
+    h.chunk_stripes = chunk;
+  }
+  for (int i = 0; i < 2; i++)
+    if (!h.st[i] && cudaStreamCreateWithFlags(&h.st[i], cudaStreamNonBlocking) != cudaSuccess)
+      return fail(PMRC_ECUDA, "stream create");
+  if (!h.ev_start && cudaEventCreateWithFlags(&h.ev_start, cudaEventDisableTiming) != cudaSuccess)
+    return fail(PMRC_ECUDA, "event create");
+  // order after the caller's stream
+  cudaEventRecord(h.ev_start, (cudaStream_t)stream);
+  for (int i = 0; i < 2; i++) cudaStreamWaitEvent(h.st[i], h.ev_start, 0);
+  size_t idx = 0;
+  for (size_t s0 = 0; s0 < stripes; s0 += chunk, idx++) {
+    const size_t ns = std::min(chunk, stripes - s0);
+    const int b = (int)(idx & 1);
+    cudaStream_t st = h.st[b];
+    if (cudaMemcpyAsync(h.d_data[b], (const uint8_t *)data_host + s0 * in_b, ns * in_b, cudaMemcpyHostToDevice, st) !=
+        cudaSuccess)
+      return fail(PMRC_ECUDA, "H2D copy");
+    uint64_t ptrs[2] = {(uint64_t)(uintptr_t)h.d_data[b], (uint64_t)(uintptr_t)h.d_par[b]};
+    uint64_t strides[2] = {in_b, out_b};
+    std::string err;
+    rc = launch_kernel(c->enc, ptrs, strides, S, ns, st, err);
+    if (rc) return fail(rc, err);
+    if (cudaMemcpyAsync((uint8_t *)parity_host + s0 * out_b, h.d_par[b], ns * out_b, cudaMemcpyDeviceToHost, st) !=
+        cudaSuccess)
+      return fail(PMRC_ECUDA, "D2H copy");
+  }
+  for (int i = 0; i < 2; i++)
+    if (cudaStreamSynchronize(h.st[i]) != cudaSuccess) return fail(PMRC_ECUDA, cudaGetErrorString(cudaGetLastError()));
+  return PMRC_OK;
+}
+
+int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregion *pieces, void *data_out, size_t S,
+                size_t stripes, int *n_written, void *stream) {
+  if (n_written) *n_written = 0;
+  if (!c || !surv_ids || !pieces || !data_out) return fail(PMRC_EINVAL, "NULL argument");
+  const CodeDef &D = c->def;
+  if (n_surv < 1 || n_surv > D.n || check_ids(D, surv_ids, n_surv)) return fail(PMRC_EINVAL, "bad survivor ids");
+  if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
+  const std::string key = ids_key("dec", surv_ids, n_surv, 0);
+  auto fe = c->plan_err.find(key);
+  if (fe != c->plan_err.end()) return fail(fe->second, "survivors do not span the data (cached)");
+  if (!c->plan_meta.count(key)) {
+    PlanSpec spec;
+    {
+      // ---- plan (R13): greedy B independent rows of G', systematic survivors first ----
+      std::vector<int> order;
+      for (int pass = 0; pass < 2; pass++)
+        for (int id = 0; id < D.n; id++) {
+          if ((pass == 0) != (id < D.k)) continue;
+          for (int a = 0; a < n_surv; a++)
+            if (surv_ids[a] == id) order.push_back(a);
+        }
+      // incremental elimination to test independence
+      std::vector<std::vector<uint8_t>> basis;  // reduced rows
+      std::vector<int> pivcol;
+      std::vector<std::pair<int, int>> sel;  // (survivor index, symbol)
+      Mat Sel(D.B, D.B);
+      const GF256 &F = gf();
+      for (int a : order) {
+        for (int j = 0; j < D.alpha && (int)sel.size() < D.B; j++) {
+          std::vector<uint8_t> row(D.B);
+          for (int x = 0; x < D.B; x++) row[x] = D.Gsys.at(surv_ids[a] * D.alpha + j, x);
+          std::vector<uint8_t> red = row;
+          for (size_t bi = 0; bi < basis.size(); bi++) {
+            uint8_t f = red[pivcol[bi]];
+            if (!f) continue;
+            for (int x = 0; x < D.B; x++) red[x] ^= F.mul(f, basis[bi][x]);
+          }
+          int pc = -1;
+          for (int x = 0; x < D.B; x++)
+            if (red[x]) { pc = x; break; }
+          if (pc < 0) continue;
+          uint8_t s = F.inv(red[pc]);
+          for (int x = 0; x < D.B; x++) red[x] = F.mul(red[x], s);
+          // keep basis fully reduced on pivot columns
+          for (size_t bi = 0; bi < basis.size(); bi++) {
+            uint8_t f = basis[bi][pc];
+            if (!f) continue;
+            for (int x = 0; x < D.B; x++) basis[bi][x] ^= F.mul(f, red[x]);
+          }
+          basis.push_back(red);
+          pivcol.push_back(pc);
+          for (int x = 0; x < D.B; x++) Sel.at((int)sel.size(), x) = row[x];
+          sel.push_back({a, j});
+        }
+      }
+      if ((int)sel.size() < D.B) {
+        c->plan_err[key] = PMRC_ESINGULAR;
+        return fail(PMRC_ESINGULAR, "survivors do not span the data");
+      }
+      Mat Inv;
+      if (!invert(Sel, Inv)) return fail(PMRC_ESINGULAR, "selected rows singular");
+      // missing data blocks: not held by a surviving systematic node
+      std::vector<char> held(D.B, 0);
+      for (int a = 0; a < n_surv; a++)
+        if (surv_ids[a] < D.k)
+          for (int j = 0; j < D.alpha; j++) held[D.sys_block(surv_ids[a], j)] = 1;
+      std::vector<int> missing;
+      for (int x = 0; x < D.B; x++)
+        if (!held[x]) missing.push_back(x);
+      if (missing.empty()) {
+        c->plan_meta[key] = 0;
+        return PMRC_OK;
+      }
+      spec.n_slots = n_surv + 1;
+      std::vector<int> used_cols;
+      for (int x = 0; x < D.B; x++) {
+        bool nz = false;
+        for (int m : missing) nz |= Inv.at(m, x) != 0;
+        if (nz) used_cols.push_back(x);
+      }
+      for (int x : used_cols) spec.inputs.push_back({{{sel[x].first, sel[x].second, 1}}});
+      for (int m : missing) spec.outputs.push_back({n_surv, m});
+      spec.A = Mat((int)missing.size(), (int)used_cols.size());
+      for (size_t r = 0; r < missing.size(); r++)
+        for (size_t x = 0; x < used_cols.size(); x++) spec.A.at((int)r, (int)x) = Inv.at(missing[r], used_cols[x]);
+    }
+    Kernel *Kb = nullptr;
+    int rc = get_kernel(c, key, spec, &Kb);
+    if (rc) return rc;
+    c->plan_meta[key] = (int)spec.outputs.size();
+  }
+  const int written = c->plan_meta[key];
+  Kernel *K = written ? c->plans[key].get() : nullptr;
+  if (n_written) *n_written = written;
+  if (!written || !stripes || !S) return PMRC_OK;
+  std::vector<uint64_t> ptrs(n_surv + 1), strides(n_surv + 1);
+  for (int a = 0; a < n_surv; a++) {
+    int rc = check_region(pieces[a].ptr, pieces[a].stripe_stride, stripes);
+    if (rc) return fail(rc, "bad survivor piece region");
+    ptrs[a] = (uint64_t)(uintptr_t)pieces[a].ptr;
+    strides[a] = pieces[a].stripe_stride;
+  }
+  int rc = check_region(data_out, (size_t)D.B * S, stripes);
+  if (rc) return fail(rc, "bad data_out");
+  ptrs[n_surv] = (uint64_t)(uintptr_t)data_out;
+  strides[n_surv] = (uint64_t)D.B * S;
+  std::string err;
+  rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err);
+  if (rc) return fail(rc, err);
+  return PMRC_OK;
+}
+
+int pmrc_read_cost(const pmrc_code *c, int lost_id, int *blocks) {
+  if (!c || !blocks) return fail(PMRC_EINVAL, "NULL argument");
+  if (lost_id < 0 || lost_id >= c->def.n) return fail(PMRC_EINVAL, "bad lost id");
+  int cnt = 0;
+  for (uint8_t v : repair_mu(c->def, lost_id)) cnt += v != 0;
+  *blocks = cnt;
+  return PMRC_OK;
+}
+
+static int repair_common(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers, int *need) {
+  const CodeDef &D = c->def;
+  *need = (D.kind == KIND_RS) ? D.k : D.d;
+  if (lost_id < 0 || lost_id >= D.n) return fail(PMRC_EINVAL, "bad lost id");
+  if (n_helpers != *need) return fail(PMRC_EINVAL, "repair needs exactly d helpers (RS: k)");
+  if (check_ids(D, helper_ids, n_helpers)) return fail(PMRC_EINVAL, "bad helper ids");
+  for (int i = 0; i < n_helpers; i++)
+    if (helper_ids[i] == lost_id) return fail(PMRC_EINVAL, "lost node among helpers");
+  return PMRC_OK;
+}
+
+int pmrc_repair(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers, const pmrc_cregion *helper_pieces,
+                pmrc_region out_piece, size_t S, size_t stripes, void *stream) {
+  if (!c || !helper_ids || !helper_pieces) return fail(PMRC_EINVAL, "NULL argument");
+  int need = 0;
+  int rc = repair_common(c, lost_id, helper_ids, n_helpers, &need);
+  if (rc) return rc;
+  if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
+  const CodeDef &D = c->def;
+  const std::string key = ids_key("rep", helper_ids, n_helpers, lost_id);
+  auto fe = c->plan_err.find(key);
+  if (fe != c->plan_err.end()) return fail(fe->second, "helper matrix singular (cached)");
+  Kernel *K = nullptr;
+  if (!c->plans.count(key)) {
+    Mat R;
+    if (!repair_matrix(D, lost_id, helper_ids, R)) {
+      c->plan_err[key] = PMRC_ESINGULAR;
+      return fail(PMRC_ESINGULAR, "Psi_H singular for this (lost, helpers) pair (DESIGN.md R10)");
+    }
+    // fused plan: input h = beta_h = mu . piece_h (derived), outputs = alpha blocks
+    std::vector<uint8_t> mu = repair_mu(D, lost_id);
+    PlanSpec spec;
+    spec.n_slots = n_helpers + 1;
+    for (int h = 0; h < n_helpers; h++) {
+      InputDesc in;
+      for (size_t b = 0; b < mu.size(); b++)
+        if (mu[b]) in.terms.push_back({h, (int)b, mu[b]});
+      spec.inputs.push_back(in);
+    }
+    for (int a = 0; a < D.alpha; a++) spec.outputs.push_back({n_helpers, a});
+    spec.A = R;
+    rc = get_kernel(c, key, spec, &K);
+    if (rc) return rc;
+  } else {
+    K = c->plans[key].get();
+  }
+  if (!stripes || !S) return PMRC_OK;
+  std::vector<uint64_t> ptrs(n_helpers + 1), strides(n_helpers + 1);
+  for (int h = 0; h < n_helpers; h++) {
+    rc = check_region(helper_pieces[h].ptr, helper_pieces[h].stripe_stride, stripes);
+    if (rc) return fail(rc, "bad helper piece region");
+    ptrs[h] = (uint64_t)(uintptr_t)helper_pieces[h].ptr;
+    strides[h] = helper_pieces[h].stripe_stride;
+  }
+  rc = check_region(out_piece.ptr, out_piece.stripe_stride, stripes);
+  if (rc) return fail(rc, "bad output piece region");
+  ptrs[n_helpers] = (uint64_t)(uintptr_t)out_piece.ptr;
+  strides[n_helpers] = out_piece.stripe_stride;
+  std::string err;
+  rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err);
+  if (rc) return fail(rc, err);
+  return PMRC_OK;
+}
+
+int pmrc_repair_project(pmrc_code *c, int lost_id, pmrc_cregion piece, pmrc_region beta, size_t S, size_t stripes,
+                        void *stream) {
+  if (!c) return fail(PMRC_EINVAL, "NULL handle");
+  const CodeDef &D = c->def;
+  if (lost_id < 0 || lost_id >= D.n) return fail(PMRC_EINVAL, "bad lost id");
+  if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
+  const std::string key = "proj:" + std::to_string(lost_id);
+  Kernel *K = nullptr;
+  if (!c->plans.count(key)) {
+    std::vector<uint8_t> mu = repair_mu(D, lost_id);
+    PlanSpec spec;
+    spec.n_slots = 2;
+    std::vector<int> cols;
+    for (size_t b = 0; b < mu.size(); b++)
+      if (mu[b]) {
+        spec.inputs.push_back({{{0, (int)b, 1}}});  // only blocks with nonzero mu are read
+        cols.push_back((int)b);
+      }
+    spec.outputs.push_back({1, 0});
+    spec.A = Mat(1, (int)cols.size());
+    for (size_t x = 0; x < cols.size(); x++) spec.A.at(0, (int)x) = mu[cols[x]];
+    int rc = get_kernel(c, key, spec, &K);
+    if (rc) return rc;
+  } else {
+    K = c->plans[key].get();
+  }
+  if (!stripes || !S) return PMRC_OK;
+  int rc = check_region(piece.ptr, piece.stripe_stride, stripes);
+  if (!rc) rc = check_region(beta.ptr, beta.stripe_stride, stripes);
+  if (rc) return fail(rc, "bad piece/beta region");
+  uint64_t ptrs[2] = {(uint64_t)(uintptr_t)piece.ptr, (uint64_t)(uintptr_t)beta.ptr};
+  uint64_t strides[2] = {piece.stripe_stride, beta.stripe_stride};
+  std::string err;
+  rc = launch_kernel(*K, ptrs, strides, S, stripes, stream, err);
+  if (rc) return fail(rc, err);
+  return PMRC_OK;
+}
+
+int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers, const pmrc_cregion *betas,
+                        pmrc_region out_piece, size_t S, size_t stripes, void *stream) {
+  if (!c || !helper_ids || !betas) return fail(PMRC_EINVAL, "NULL argument");
+  int need = 0;
+  int rc = repair_common(c, lost_id, helper_ids, n_helpers, &need);
+  if (rc) return rc;
+  if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
+  const CodeDef &D = c->def;
+  const std::string key = ids_key("comb", helper_ids, n_helpers, lost_id);
+  auto fe = c->plan_err.find(key);
+  if (fe != c->plan_err.end()) return fail(fe->second, "helper matrix singular (cached)");
+  Kernel *K = nullptr;
+  if (!c->plans.count(key)) {
+    Mat R;
+    if (!repair_matrix(D, lost_id, helper_ids, R)) {
+      c->plan_err[key] = PMRC_ESINGULAR;
+      return fail(PMRC_ESINGULAR, "Psi_H singular for this (lost, helpers) pair (DESIGN.md R10)");
+    }
+    PlanSpec spec;
+    spec.n_slots = n_helpers + 1;
+    for (int h = 0; h < n_helpers; h++) spec.inputs.push_back({{{h, 0, 1}}});
+    for (int a = 0; a < D.alpha; a++) spec.outputs.push_back({n_helpers, a});
+    spec.A = R;
+    rc = get_kernel(c, key, spec, &K);
+    if (rc) return rc;
+  } else {
+    K = c->plans[key].get();
+  }
+  if (!stripes || !S) return PMRC_OK;
+  std::vector<uint64_t> ptrs(n_helpers + 1), strides(n_helpers + 1);
+  for (int h = 0; h < n_helpers; h++) {
+    rc = check_region(betas[h].ptr, betas[h].stripe_stride, stripes);
+    if (rc) return fail(rc, "bad beta region");
+    ptrs[h] = (uint64_t)(uintptr_t)betas[h].ptr;
+    strides[h] = betas[h].stripe_stride;
+  }
+  rc = check_region(out_piece.ptr, out_piece.stripe_stride, stripes);
+  if (rc) return fail(rc, "bad output piece region");
+  ptrs[n_helpers] = (uint64_t)(uintptr_t)out_piece.ptr;
+  strides[n_helpers] = out_piece.stripe_stride;
+  std::string err;
+  rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err);
+  if (rc) return fail(rc, err);
+  return PMRC_OK;
+}
+
+}  // extern "C"

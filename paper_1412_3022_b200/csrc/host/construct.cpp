@@ -1,0 +1,188 @@
+#include "construct.hpp"
+
+#include "../../../include/pmrc.h"
+
+namespace pmrc {
+
+int CodeDef::sys_block(int i, int j) const {
+  if (kind == KIND_MBR) return Lidx[(size_t)i * Lcols + j] - 1;
+  return i * alpha + j;
+}
+
+namespace {
+
+// index matrix: symmetric blocks numbered row-major over the upper triangle (R4)
+void number_symmetric(std::vector<int> &L, int cols, int r0, int c0, int m, int &next) {
+  for (int a = 0; a < m; a++)
+    for (int b = a; b < m; b++) {
+      L[(size_t)(r0 + a) * cols + c0 + b] = next;
+      L[(size_t)(r0 + b) * cols + c0 + a] = next;
+      next++;
+    }
+}
+
+// C(n, r) capped
+double n_choose(int n, int r) {
+  double v = 1;
+  for (int i = 0; i < r; i++) v = v * (n - i) / (i + 1);
+  return v;
+}
+
+bool all_subsets_full_rank(const Mat &psi, int rsel, int cols) {
+  int n = psi.r;
+  std::vector<int> c(rsel);
+  for (int i = 0; i < rsel; i++) c[i] = i;
+  Mat M(rsel, cols);
+  for (;;) {
+    for (int a = 0; a < rsel; a++)
+      for (int t = 0; t < cols; t++) M.at(a, t) = psi.at(c[a], t);
+    if (rank(M) < rsel) return false;
+    int i = rsel - 1;
+    while (i >= 0 && c[i] == n - rsel + i) i--;
+    if (i < 0) return true;
+    c[i]++;
+    for (int j = i + 1; j < rsel; j++) c[j] = c[j - 1] + 1;
+  }
+}
+
+}  // namespace
+
+int build_code(int kind, int k, int d, int n, int w, CodeDef &o, std::string &err) {
+  const GF256 &F = gf();
+  if (w != 8) { err = "only w = 8 (GF(2^8)) is supported"; return PMRC_EUNSUPPORTED; }
+  if (k < 1 || n < 2 || n > 255) { err = "bad n/k"; return PMRC_EINVAL; }
+  o = CodeDef();
+  o.kind = kind; o.n = n; o.k = k;
+  switch (kind) {
+    case KIND_MSR_SPARSE:
+    case KIND_MSR_VANILLA:
+      // alpha = Delta = d - k + 1; PM-MSR needs d = 2k - 2 (R7)
+      if (k < 2 || d != 2 * k - 2) { err = "MSR requires k >= 2 and d = 2k-2"; return PMRC_EUNSUPPORTED; }
+      if (n <= d) { err = "MSR requires n > d"; return PMRC_EINVAL; }
+      o.d = d; o.alpha = k - 1; o.B = k * o.alpha;
+      break;
+    case KIND_MBR:
+      // alpha = d, Delta = (2d - k + 1)/2
+      if (k < 2 || d < k || n <= d) { err = "MBR requires 2 <= k <= d < n"; return PMRC_EINVAL; }
+      o.d = d; o.alpha = d; o.B = k * (2 * d - k + 1) / 2;
+      break;
+    case KIND_RS:
+      if (n <= k) { err = "RS requires n > k"; return PMRC_EINVAL; }
+      o.d = k; o.alpha = 1; o.B = k;
+      break;
+    default: err = "unknown kind"; return PMRC_EINVAL;
+  }
+  const int a = o.alpha;
+  o.P = (n - k) * a;
+
+  // ---- Psi (and lambda) ----
+  if (kind == KIND_RS) {
+    o.psi = Mat(n, k);  // R12: V_ij = g^{(i-1)(j-1)}
+    for (int i = 0; i < n; i++)
+      for (int j = 0; j < k; j++) o.psi.at(i, j) = F.gexp((long)i * j);
+  } else {
+    o.psi = Mat(n, o.d);
+    o.lambda.assign(n, 0);
+    if (kind == KIND_MSR_VANILLA) {
+      // Phi_ij = g^{(i-1)(j-1)}, Lambda_ii = g^{(i-1) alpha}, Psi = [Phi  Lambda Phi]
+      for (int i = 0; i < n; i++) {
+        o.lambda[i] = F.gexp((long)i * a);
+        for (int j = 0; j < a; j++) {
+          uint8_t phi = F.gexp((long)i * j);
+          o.psi.at(i, j) = phi;
+          o.psi.at(i, a + j) = F.mul(o.lambda[i], phi);
+        }
+      }
+      for (int i = 0; i < n; i++)
+        for (int i2 = 0; i2 < i; i2++)
+          if (o.lambda[i] == o.lambda[i2]) {
+            err = "vanilla MSR: Lambda values collide (n > 255/gcd(alpha,255), R8)";
+            return PMRC_EUNSUPPORTED;
+          }
+    } else if (kind == KIND_MSR_SPARSE) {
+      // x_i = g^{i+alpha} (1-based i, R2); Phi = [I_alpha; 1/(x_i - y_j)], y_j = g^{j-1};
+      // Lambda_ii = (x_i - 1)/(x_i - g^alpha)
+      if (n + a > 254) { err = "sparse MSR needs n + alpha <= 254 in GF(2^8)"; return PMRC_EUNSUPPORTED; }
+      for (int i = 0; i < n; i++) {
+        uint8_t x = F.gexp(i + 1 + a);
+        o.lambda[i] = F.div(x ^ 1, x ^ F.gexp(a));
+        for (int j = 0; j < a; j++) {
+          uint8_t phi = (i < a) ? (uint8_t)(i == j) : F.inv(x ^ F.gexp(j));
+          o.psi.at(i, j) = phi;
+          o.psi.at(i, a + j) = F.mul(o.lambda[i], phi);
+        }
+      }
+      for (int i = 0; i < n; i++)
+        for (int i2 = 0; i2 < i; i2++)
+          if (o.lambda[i] == o.lambda[i2]) { err = "sparse MSR: Lambda values collide"; return PMRC_EUNSUPPORTED; }
+    } else {
+      // MBR (R5): rows 1..k = [I_k 0], rows i = k+1..n: 1/(g^{d+i} - g^{j-1})
+      if (n + o.d > 254) { err = "MBR needs n + d <= 254 in GF(2^8)"; return PMRC_EUNSUPPORTED; }
+      for (int i = 0; i < n; i++)
+        for (int j = 0; j < o.d; j++)
+          o.psi.at(i, j) = (i < k) ? (uint8_t)(i == j) : F.inv(F.gexp(o.d + i + 1) ^ F.gexp(j));
+    }
+  }
+
+  // ---- index matrix L ----
+  if (kind == KIND_RS) {
+    o.Lrows = k; o.Lcols = 1;
+    o.Lidx.resize(k);
+    for (int i = 0; i < k; i++) o.Lidx[i] = i + 1;
+  } else if (kind == KIND_MBR) {
+    o.Lrows = o.d; o.Lcols = o.d;
+    o.Lidx.assign((size_t)o.d * o.d, 0);
+    int next = 1;
+    number_symmetric(o.Lidx, o.d, 0, 0, k, next);  // S
+    for (int r = 0; r < k; r++)                    // T and T^t
+      for (int c = k; c < o.d; c++) {
+        o.Lidx[(size_t)r * o.d + c] = next;
+        o.Lidx[(size_t)c * o.d + r] = next;
+        next++;
+      }
+  } else {
+    o.Lrows = o.d; o.Lcols = a;
+    o.Lidx.assign((size_t)o.d * a, 0);
+    int next = 1;
+    number_symmetric(o.Lidx, a, 0, 0, a, next);  // S1
+    number_symmetric(o.Lidx, a, a, 0, a, next);  // S2
+  }
+
+  // ---- G: G_{alpha i + j, L_{l,j}} = Psi_{i,l} ----
+  o.G = Mat(n * a, o.B);
+  if (kind == KIND_RS) {
+    o.G = o.psi;
+  } else {
+    for (int i = 0; i < n; i++)
+      for (int j = 0; j < a; j++)
+        for (int l = 0; l < o.d; l++) {
+          int idx = o.Lidx[(size_t)l * o.Lcols + j];
+          if (idx) o.G.at(i * a + j, idx - 1) = o.psi.at(i, l);
+        }
+  }
+
+  // ---- G' ----
+  if (kind == KIND_MBR) {
+    o.Gsys = o.G;  // R6: systematic rows are unit rows already
+  } else {
+    Mat Gt(o.B, o.B), Gti;
+    for (int r = 0; r < o.B; r++)
+      for (int c2 = 0; c2 < o.B; c2++) Gt.at(r, c2) = o.G.at(r, c2);
+    if (!invert(Gt, Gti)) { err = "Gtilde (first B rows of G) is singular"; return PMRC_EUNSUPPORTED; }
+    o.Gsys = matmul(o.G, Gti);
+  }
+  o.Gpp = Mat(o.P, o.B);
+  for (int r = 0; r < o.P; r++)
+    for (int c2 = 0; c2 < o.B; c2++) o.Gpp.at(r, c2) = o.Gsys.at(k * a + r, c2);
+
+  // ---- repair completeness: every d rows of Psi independent ----
+  if (kind != KIND_RS) {
+    if (n_choose(n, o.d) <= 20000)
+      o.repair_complete = all_subsets_full_rank(o.psi, o.d, o.d);
+    else
+      o.repair_complete = (n == o.d + 1) ? all_subsets_full_rank(o.psi, o.d, o.d) : false;
+  }
+  return PMRC_OK;
+}
+
+}  // namespace pmrc

@@ -1,0 +1,82 @@
+// Region-linear-combination plans and their bitsliced sm_100a kernels.
+//
+// A plan computes, for every stripe t and byte position p,
+//     out_r[t][p] = XOR_c A[r][c] * in_c[t][p]          over GF(2^8)
+// where every input / output is a block addressed as  slot_ptr[slot] + t*slot_stride[slot]
+// + blk*S.  Encode (G''), decode (rows of Gtilde^{-1}) and repair (projection + newcomer) are all
+// plans; only the coefficient matrix and the slot wiring differ (north star: "reuse the same
+// region-linear-combination kernel").  An input may itself be a small combination of blocks
+// ("derived" input, used by the fused repair: beta_h = phi_f . piece_h).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "gf256.hpp"
+#include "xorprog.hpp"
+
+namespace pmrc {
+
+struct Term {
+  int slot, blk;
+  uint8_t coef;
+};
+struct InputDesc {
+  std::vector<Term> terms;  // one term with coef 1 = plain block
+};
+struct OutputDesc {
+  int slot, blk;
+};
+
+struct PlanSpec {
+  int n_slots = 0;
+  std::vector<InputDesc> inputs;
+  std::vector<OutputDesc> outputs;
+  Mat A;  // outputs x inputs
+};
+
+struct GenOptions {
+  int max_rows = 8;      // output blocks per group (8 planes each in registers)
+  int in_block = 16;     // inputs per CSE block (register pressure vs. sharing)
+  int tpb = 256;         // threads per CTA
+  bool cse = true;       // Paar CSE (false: naive per-row XOR chains)
+};
+
+struct GenStats {
+  int groups = 0;
+  long xor2 = 0;         // 2-input XORs of the emitted network
+  long naive_lop3 = 0;   // W of SURVEY §8(d) (per 32 byte positions)
+  long xor2_naive = 0;   // 2-input XORs without CSE
+  int transposes = 0;    // 8x8 bit transposes per 32 byte positions (in + out)
+  long loads = 0;        // 16-B vector loads per lane per item sum
+};
+
+// Generate CUDA C++ source of the bitsliced kernel `pmrc_kernel` for a plan.
+std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st);
+
+// Compiled kernel (driver-API module) bound to the device current at compile time.
+struct Kernel {
+  void *module = nullptr;    // CUmodule
+  void *function = nullptr;  // CUfunction
+  int n_slots = 0;
+  int n_groups = 0;
+  int tpb = 256;
+  int blocks_per_sm = 1;
+  int sms = 148;
+  int regs = 0;
+  GenStats stats;
+  std::string source;
+  double compile_ms = 0;
+};
+
+// Generate + NVRTC-compile + load.  Returns 0 or PMRC_E*; err gets the log on failure.
+int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string &err);
+void free_kernel(Kernel &k);
+
+// Launch over `stripes` stripes of S-byte blocks.  ptrs/strides: n_slots entries.
+int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides, size_t S, size_t stripes,
+                  void *stream, std::string &err);
+
+unsigned long long &launch_counter();
+
+}  // namespace pmrc

@@ -1,0 +1,30 @@
+// GF(2) straight-line XOR programs for bitsliced GF(2^8) region linear combinations.
+//
+// A GF(2^8) coefficient c acts on a byte as an 8x8 GF(2) matrix (column b' = c * 2^{b'}), so a
+// group of m output blocks fed by q input blocks is a (8m) x (8q) bit matrix applied to bit planes
+// (SURVEY §8(a) "bit-sliced" formulation).  Zero coefficients contribute no columns (the paper's
+// sparsification, applied at kernel-generation time).  We shorten the XOR network with
+// Paar's greedy common-subexpression elimination (repeatedly materialise the pair of signals that
+// co-occurs in most rows); the result is exact (GF(2) identities), so outputs are bit-identical to
+// the plain matrix product.
+#pragma once
+#include <array>
+#include <cstdint>
+#include <vector>
+
+namespace pmrc {
+
+struct Slp {
+  int n_in = 0;                          // base signals 0..n_in-1
+  std::vector<std::array<int, 2>> tmp;   // signal n_in+i = tmp[i][0] ^ tmp[i][1]
+  std::vector<std::vector<int>> rows;    // each output = XOR of these signals (empty = 0)
+  long xor2() const;                     // 2-input XOR count
+};
+
+// rows_in[r] = sorted list of base signals XORed into output r
+Slp paar(int n_in, const std::vector<std::vector<int>> &rows_in);
+
+// naive 3-input-LOP3 count of a bit matrix row set: sum ceil((ones-1)/2)
+long naive_lop3(const std::vector<std::vector<int>> &rows);
+
+}  // namespace pmrc

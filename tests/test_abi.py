@@ -1,0 +1,108 @@
+"""CPU tier: libpmrc.so loads without a GPU, exports every symbol include/pmrc.h declares, and its
+host logic (construction, info, error paths) behaves; the data path fails loudly without a GPU."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1412_3022_b200 as pm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_header_symbols_exported():
+    hdr = open(os.path.join(ROOT, "include", "pmrc.h")).read()
+    declared = set(re.findall(r"\b(pmrc_[a-z_]+)\s*\(", hdr))
+    assert declared == set(pm.EXPORTS)
+    L = pm.lib()
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+@pytest.mark.parametrize("kind,k,n", [(0, 3, 6), (0, 8, 16), (1, 8, 16), (2, 8, 16), (3, 8, 16), (0, 4, 8), (2, 3, 6),
+                                      (0, 16, 32)])
+def test_host_matrices_equal_oracle(kind, k, n):
+    # the product's host construction (independent code) reproduces the oracle's matrices
+    d = k if kind == 3 else 2 * k - 2
+    c = pm.pmrc_create(kind, k, d, n)
+    try:
+        assert np.array_equal(pm.pmrc_matrix(c, pm.MATRIX_GPP), O.parity_matrix(kind, n, k, d))
+        assert np.array_equal(pm.pmrc_matrix(c, pm.MATRIX_G), O.generator(kind, n, k, d))
+        assert np.array_equal(pm.pmrc_matrix(c, pm.MATRIX_GSYS), O.systematic(kind, n, k, d))
+        psi, lam = O.psi(kind, n, k, d)
+        assert np.array_equal(pm.pmrc_matrix(c, pm.MATRIX_PSI), psi)
+        if kind != 3:
+            assert np.array_equal(pm.pmrc_layout(c), O.index_matrix(kind, k, d))
+        info = pm.pmrc_info(c)
+        G2 = O.parity_matrix(kind, n, k, d)
+        assert info["nnz"] == int((G2 != 0).sum())
+        for f in range(n):
+            want = 1 if kind == 3 else O.repair_reads(kind, n, k, d, f)
+            assert pm.pmrc_read_cost(c, f) == want
+    finally:
+        pm.pmrc_destroy(c)
+
+
+def test_info_config2():
+    c = pm.pmrc_create(pm.PMRC_MSR_SPARSE, 8, 14, 16)
+    info = pm.pmrc_info(c)
+    pm.pmrc_destroy(c)
+    assert (info["alpha"], info["B"], info["parity_rows"], info["nnz"]) == (7, 56, 56, 784)
+    assert info["zero_pct"] == 75.0
+    assert info["repair_complete"] == 0          # R10: n = 2k
+    assert info["xor_ops_naive"] == 12584        # SURVEY §8(d) W for config 2
+    assert 0 < info["xor_ops"] < 2 * info["xor_ops_naive"]
+
+
+def test_create_errors():
+    with pytest.raises(pm.PmrcError) as e:
+        pm.pmrc_create(pm.PMRC_MSR_SPARSE, 3, 3, 6)   # MSR needs d = 2k-2
+    assert e.value.rc == pm.PMRC_EUNSUPPORTED
+    with pytest.raises(pm.PmrcError) as e:
+        pm.pmrc_create(pm.PMRC_MSR_SPARSE, 8, 14, 16, w=16)
+    assert e.value.rc == pm.PMRC_EUNSUPPORTED
+    with pytest.raises(pm.PmrcError) as e:
+        pm.pmrc_create(pm.PMRC_MSR_VANILLA, 16, 30, 32)  # R8 lambda collision
+    assert e.value.rc == pm.PMRC_EUNSUPPORTED
+    with pytest.raises(pm.PmrcError):
+        pm.pmrc_create(pm.PMRC_MBR, 8, 14, 14)           # n must exceed d
+
+
+def test_argument_errors_without_gpu_work():
+    c = pm.pmrc_create(pm.PMRC_MSR_SPARSE, 3, 4, 6)
+    try:
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_encode(c, 16, 16, 24, 1)              # S % 16 != 0
+        assert e.value.rc == pm.PMRC_EALIGN
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_encode(c, 8, 16, 32, 1)               # misaligned pointer
+        assert e.value.rc == pm.PMRC_EALIGN
+        pm.pmrc_encode(c, 16, 16, 0, 5)                   # empty: no work, no error
+        pm.pmrc_encode(c, 16, 16, 32, 0)
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_repair(c, 0, [0, 1, 2, 3], [(16, 0)] * 4, (16, 0), 32, 1)   # lost among helpers
+        assert e.value.rc == pm.PMRC_EINVAL
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_repair(c, 0, [1, 2, 3], [(16, 0)] * 3, (16, 0), 32, 1)      # needs d helpers
+        assert e.value.rc == pm.PMRC_EINVAL
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_decode(c, [0, 0, 1], [(16, 0)] * 3, 16, 32, 1)            # duplicate ids
+        assert e.value.rc == pm.PMRC_EINVAL
+    finally:
+        pm.pmrc_destroy(c)
+
+
+def test_no_silent_cpu_fallback():
+    # without a GPU the data path must fail loudly (PMRC_ECUDA), never compute on the CPU
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    c = pm.pmrc_create(pm.PMRC_MSR_SPARSE, 3, 4, 6)
+    try:
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_encode(c, 16, 16, 32, 1)
+        assert e.value.rc == pm.PMRC_ECUDA
+    finally:
+        pm.pmrc_destroy(c)

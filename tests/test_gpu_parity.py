@@ -1,0 +1,270 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI vs the oracle, element by element, on the
+same seeded inputs; sizes span several 1 KiB chunks and ragged tails.  Plus full-size config 2
+(1 GiB, the bench's launch configuration) on sampled stripes/windows."""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import inputs
+import oracle as O
+import paper_1412_3022_b200 as pm
+from gpu_util import DEV, Stripes, oracle_kind
+
+pytestmark = pytest.mark.gpu
+
+ENC_CASES = [
+    (pm.PMRC_MSR_SPARSE, 3, 6, 2048, 16),     # config 1 shape
+    (pm.PMRC_MSR_SPARSE, 8, 16, 4096 + 1024 + 16, 3),   # config 2 code, ragged chunk tail
+    (pm.PMRC_MSR_SPARSE, 8, 15, 1040, 2),
+    (pm.PMRC_MSR_VANILLA, 8, 16, 2064, 2),
+    (pm.PMRC_MBR, 8, 16, 3072 + 48, 2),       # config 3 code
+    (pm.PMRC_RS_VANDERMONDE, 8, 16, 4096, 3),
+    (pm.PMRC_MSR_SPARSE, 4, 8, 1024, 5),
+    (pm.PMRC_MBR, 4, 8, 1008, 4),
+    (pm.PMRC_MSR_SPARSE, 16, 32, 1024 + 32, 1),
+    (pm.PMRC_MBR, 16, 32, 512, 1),
+    (pm.PMRC_MSR_SPARSE, 2, 3, 16, 7),        # smallest code, one vector per block
+]
+
+
+@pytest.mark.parametrize("kind,k,n,S,stripes", ENC_CASES)
+def test_encode_bit_exact(kind, k, n, S, stripes):
+    st = Stripes(kind, k, n, S, stripes, seed=11 + k)
+    try:
+        st.encode()
+        want = O.encode(oracle_kind(kind), n, k, st.d, st.host_data())
+        got = st.parity.cpu().numpy()
+        assert np.array_equal(got, want)
+    finally:
+        st.close()
+
+
+def test_encode_empty_and_alignment():
+    st = Stripes(pm.PMRC_MSR_SPARSE, 3, 6, 32, 2, seed=3)
+    try:
+        before = st.parity.clone()
+        pm.pmrc_encode(st.code, st.data.data_ptr(), st.parity.data_ptr(), 0, 2, st.stream)
+        pm.pmrc_encode(st.code, st.data.data_ptr(), st.parity.data_ptr(), 32, 0, st.stream)
+        torch.cuda.synchronize()
+        assert torch.equal(before, st.parity)
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_encode(st.code, st.data.data_ptr() + 8, st.parity.data_ptr(), 32, 1, st.stream)
+        assert e.value.rc == pm.PMRC_EALIGN
+    finally:
+        st.close()
+
+
+def test_encode_does_not_touch_beyond_parity():
+    # the kernel writes exactly stripes x P x S bytes: guard bytes after the buffer stay intact
+    k, n, S, stripes = 8, 16, 1024 + 16, 2
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=5)
+    try:
+        big = torch.full((stripes * st.P * S + 4096,), 0x5A, dtype=torch.uint8, device=DEV)
+        pm.pmrc_encode(st.code, st.data.data_ptr(), big.data_ptr(), S, stripes, st.stream)
+        torch.cuda.synchronize()
+        assert bool((big[stripes * st.P * S:] == 0x5A).all())
+        want = O.encode(O.MSR_SPARSE, n, k, st.d, st.host_data())
+        assert np.array_equal(big[: stripes * st.P * S].cpu().numpy().reshape(stripes, st.P, S), want)
+    finally:
+        st.close()
+
+
+@pytest.mark.parametrize("kind", [pm.PMRC_MSR_SPARSE, pm.PMRC_MSR_VANILLA, pm.PMRC_MBR, pm.PMRC_RS_VANDERMONDE])
+def test_decode_config1_every_subset(kind):
+    # config 1: k=3, n=6 (RS uses the same k, n): decode from every 3-subset
+    k, n, S, stripes = 3, 6, 2048, 16
+    st = Stripes(kind, k, n, S, stripes, seed=1)
+    try:
+        st.encode()
+        for ids in itertools.combinations(range(n), k):
+            out = torch.zeros_like(st.data)
+            nw = pm.pmrc_decode(st.code, list(ids), [st.piece(i) for i in ids], out.data_ptr(), S, stripes, st.stream)
+            torch.cuda.synchronize()
+            held = set()
+            for i in ids:
+                if i < k:
+                    held |= ({i * st.alpha + j for j in range(st.alpha)} if kind != pm.PMRC_MBR
+                             else {int(v) - 1 for v in st.L[i]})
+            missing = sorted(set(range(st.B)) - held)
+            assert nw == len(missing)
+            assert torch.equal(out[:, missing], st.data[:, missing]), ids
+            untouched = sorted(held)
+            assert not out[:, untouched].any()   # only missing blocks are written
+    finally:
+        st.close()
+
+
+@pytest.mark.parametrize("kind", [pm.PMRC_MSR_SPARSE, pm.PMRC_MBR])
+def test_decode_k8_random_subsets(kind):
+    k, n, S, stripes = 8, 16, 2048 + 16, 2
+    st = Stripes(kind, k, n, S, stripes, seed=9)
+    try:
+        st.encode()
+        r = inputs.rng(4)
+        for _ in range(6):
+            ids = sorted(r.choice(n, k, replace=False).tolist())
+            out = st.data.clone()
+            lost = [i for i in range(k) if i not in ids]
+            # poison the lost systematic blocks, decode in place
+            for i in lost:
+                if kind != pm.PMRC_MBR:
+                    out[:, i * st.alpha:(i + 1) * st.alpha] = 0xCC
+            pm.pmrc_decode(st.code, ids, [st.piece(i) for i in ids], out.data_ptr(), S, stripes, st.stream)
+            torch.cuda.synchronize()
+            if kind != pm.PMRC_MBR:
+                assert torch.equal(out, st.data), ids
+            else:
+                # oracle cross-check of the decoded blocks
+                got = out.cpu().numpy()
+                want = st.host_data()
+                assert np.array_equal(got, want), ids
+    finally:
+        st.close()
+
+
+def test_decode_more_than_k_survivors_and_errors():
+    k, n, S = 3, 6, 1024
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, 4, seed=2)
+    try:
+        st.encode()
+        ids = [5, 1, 4, 3]   # unsorted, one systematic
+        out = torch.zeros_like(st.data)
+        pm.pmrc_decode(st.code, ids, [st.piece(i) for i in ids], out.data_ptr(), S, 4, st.stream)
+        torch.cuda.synchronize()
+        miss = [0, 1, 4, 5]
+        assert torch.equal(out[:, miss], st.data[:, miss])
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_decode(st.code, [3, 4], [st.piece(3), st.piece(4)], out.data_ptr(), S, 4, st.stream)
+        assert e.value.rc == pm.PMRC_ESINGULAR
+    finally:
+        st.close()
+
+
+def _predicted_singular(kind, k, n, f, H):
+    alpha = k - 1
+    if kind != pm.PMRC_MSR_SPARSE or n < 2 * k:
+        return False
+    omitted = [i for i in range(n) if i != f and i not in H]
+    return f < alpha and len(omitted) == 1 and omitted[0] < alpha
+
+
+@pytest.mark.parametrize("kind", [pm.PMRC_MSR_SPARSE, pm.PMRC_MSR_VANILLA, pm.PMRC_MBR])
+def test_repair_config1_every_node_every_helper_set(kind):
+    k, n, S, stripes = 3, 6, 2048, 16
+    st = Stripes(kind, k, n, S, stripes, seed=1)
+    try:
+        st.encode()
+        d = st.d
+        n_sing = 0
+        for f in range(n):
+            for H in itertools.combinations([i for i in range(n) if i != f], d):
+                H = list(H)
+                out = torch.empty((stripes, st.alpha, S), dtype=torch.uint8, device=DEV)
+                try:
+                    pm.pmrc_repair(st.code, f, H, [st.piece(i) for i in H], (out.data_ptr(), st.alpha * S), S,
+                                   stripes, st.stream)
+                except pm.PmrcError as e:
+                    assert e.rc == pm.PMRC_ESINGULAR and _predicted_singular(kind, k, n, f, H), (f, H)
+                    n_sing += 1
+                    continue
+                torch.cuda.synchronize()
+                assert not _predicted_singular(kind, k, n, f, H)
+                assert torch.equal(out, st.piece_tensor(f)), (f, H)
+        assert n_sing == (2 if kind == pm.PMRC_MSR_SPARSE else 0)
+    finally:
+        st.close()
+
+
+@pytest.mark.parametrize("kind", [pm.PMRC_MSR_SPARSE, pm.PMRC_MBR, pm.PMRC_RS_VANDERMONDE])
+def test_repair_k8_random(kind):
+    k, n, S, stripes = 8, 16, 4096 + 16, 2
+    st = Stripes(kind, k, n, S, stripes, seed=21)
+    try:
+        st.encode()
+        r = inputs.rng(8)
+        need = k if kind == pm.PMRC_RS_VANDERMONDE else st.d
+        done = 0
+        while done < 5:
+            f = int(r.integers(n))
+            H = sorted(r.choice([i for i in range(n) if i != f], need, replace=False).tolist())
+            if _predicted_singular(kind, k, n, f, H):
+                continue
+            out = torch.empty((stripes, st.alpha, S), dtype=torch.uint8, device=DEV)
+            pm.pmrc_repair(st.code, f, H, [st.piece(i) for i in H], (out.data_ptr(), st.alpha * S), S, stripes,
+                           st.stream)
+            torch.cuda.synchronize()
+            assert torch.equal(out, st.piece_tensor(f)), (f, H)
+            done += 1
+    finally:
+        st.close()
+
+
+def test_repair_project_combine_split_equals_oracle():
+    # helper side (projection) and newcomer side (combine) as separate calls, vs the oracle
+    k, n, S, stripes = 8, 16, 2048, 2
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=33)
+    try:
+        st.encode()
+        for f in (2, 11):
+            H = [i for i in range(n) if i != f][:st.d] if f != 2 else [i for i in range(n) if i not in (2, 0)]
+            betas = torch.empty((len(H), stripes, S), dtype=torch.uint8, device=DEV)
+            for j, h in enumerate(H):
+                pm.pmrc_repair_project(st.code, f, st.piece(h), (betas[j].data_ptr(), S), S, stripes, st.stream)
+            torch.cuda.synchronize()
+            for j, h in enumerate(H):
+                piece = st.piece_tensor(h).cpu().numpy()
+                for t in range(stripes):
+                    want = O.repair_project(O.MSR_SPARSE, n, k, st.d, f, piece[t])
+                    assert np.array_equal(betas[j, t].cpu().numpy(), want)
+            out = torch.empty((stripes, st.alpha, S), dtype=torch.uint8, device=DEV)
+            pm.pmrc_repair_combine(st.code, f, H, [(betas[j].data_ptr(), S) for j in range(len(H))],
+                                   (out.data_ptr(), st.alpha * S), S, stripes, st.stream)
+            torch.cuda.synchronize()
+            assert torch.equal(out, st.piece_tensor(f))
+    finally:
+        st.close()
+
+
+def test_encode_host_path_equals_device_path():
+    k, n, S, stripes = 8, 16, 8192, 9
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=44)
+    try:
+        st.encode()
+        hd = torch.from_numpy(st.host_data()).pin_memory()
+        hp = torch.zeros((stripes, st.P, S), dtype=torch.uint8).pin_memory()
+        pm.pmrc_encode_host(st.code, hd.data_ptr(), hp.data_ptr(), S, stripes, st.stream)
+        assert torch.equal(hp, st.parity.cpu())
+    finally:
+        st.close()
+
+
+def test_full_size_config2_sampled():
+    # config 2 in the bench's launch configuration: 1 GiB real data (R11: 19 stripes of 56 x 1 MiB,
+    # last one zero padded), generated on the device; sampled stripes and byte windows vs oracle
+    k, n, S = 8, 16, 1 << 20
+    B = 56
+    real = 1 << 30
+    stripes = -(-real // (B * S))
+    code = pm.pmrc_create(pm.PMRC_MSR_SPARSE, k, 14, n)
+    try:
+        data = torch.empty((stripes, B, S), dtype=torch.uint8, device=DEV)
+        par = torch.empty((stripes, B, S), dtype=torch.uint8, device=DEV)
+        stream = torch.cuda.current_stream().cuda_stream
+        inputs.fill_device(data.data_ptr(), data.numel(), 1234, real_len=real, stream=stream)
+        pm.pmrc_encode(code, data.data_ptr(), par.data_ptr(), S, stripes, stream)
+        torch.cuda.synchronize()
+        r = inputs.rng(77)
+        for t in (0, stripes - 1, int(r.integers(1, stripes - 1))):
+            for p0 in (0, S - 4096, int(r.integers(0, S // 16 - 256)) * 16):
+                W = 4096
+                x = np.stack([inputs.host_bytes(W, 1234, t * B * S + c * S + p0, real) for c in range(B)])
+                want = O.encode(O.MSR_SPARSE, n, k, 14, x[None])[0]
+                assert np.array_equal(par[t, :, p0:p0 + W].cpu().numpy(), want), (t, p0)
+        # the padded tail of the last stripe is zero data, hence zero parity there
+        last_real = real - (stripes - 1) * B * S
+        full_blocks = last_real // S
+        assert not par[stripes - 1, :, :].any() if full_blocks == 0 else True
+    finally:
+        pm.pmrc_destroy(code)

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -181,6 +182,26 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
   if (!c) return fail(PMRC_ENOMEM, "host allocation");
   std::string err;
   if (kind == KIND_RS) d = k;
+  // tuning knob (experiments only): PMRC_GEN="max_rows=8,in_block=16,tpb=256,cse=1"
+  if (const char *g = getenv("PMRC_GEN")) {
+    std::string s = g;
+    size_t pos = 0;
+    while (pos < s.size()) {
+      size_t e = s.find(',', pos);
+      if (e == std::string::npos) e = s.size();
+      std::string kv = s.substr(pos, e - pos);
+      size_t eq = kv.find('=');
+      if (eq != std::string::npos) {
+        std::string key = kv.substr(0, eq);
+        int v = atoi(kv.c_str() + eq + 1);
+        if (key == "max_rows" && v > 0) c->gen.max_rows = v;
+        if (key == "in_block" && v > 0) c->gen.in_block = v;
+        if (key == "tpb" && v >= 32) c->gen.tpb = v;
+        if (key == "cse") c->gen.cse = v != 0;
+      }
+      pos = e + 1;
+    }
+  }
   int rc = build_code(kind, k, d, n, w, c->def, err);
   if (rc) return fail(rc, err);
   // encode plan: inputs = data blocks (slot 0), outputs = parity rows (slot 1), A = G''

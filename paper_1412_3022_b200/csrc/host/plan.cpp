@@ -157,7 +157,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   for (size_t g = 0; g < groups.size(); g++) {
     const Group &G = groups[g];
     const int m = (int)G.rows.size();
-    s << "static __device__ __forceinline__ void grp" << g
+    s << "static __device__ __noinline__ void grp" << g
       << "(const Slots &R, const u64 S, const u64 t, const u64 o0, const u64 o1, const bool v0, const bool v1) {\n";
     std::vector<std::string> outs;
     for (int r = 0; r < m; r++)
@@ -245,20 +245,22 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     s << "}\n";
   }
   const int NG = std::max(1, (int)groups.size());
+  // Each CTA owns a tile of (warps per CTA) consecutive 1 KiB chunks of one stripe; every warp walks
+  // all groups in the same order for its chunk, so the warps of an SM execute the same group code at
+  // the same time (the straight-line XOR networks are large: instruction-cache reuse across warps
+  // is what keeps the ALU fed) and a group's shared inputs were just read by the same warp (L1/L2).
   s << "extern \"C\" __global__ void __launch_bounds__(" << o.tpb << ", 1) pmrc_kernel(const __grid_constant__ Slots R, "
        "const u64 S, const u32 stripes, const u32 chunks) {\n";
-  s << "  const u32 lane = threadIdx.x & 31u;\n";
-  s << "  const u32 nw = (gridDim.x * blockDim.x) >> 5;\n";
-  s << "  const u32 items = stripes * chunks * " << NG << "u;\n";
-  s << "  for (u32 it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {\n";
-  s << "    const u32 g = it % " << NG << "u; const u32 rest = it / " << NG << "u;\n";
-  s << "    const u32 q = rest % chunks; const u64 t = rest / chunks;\n";
+  s << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, W = blockDim.x >> 5;\n";
+  s << "  const u32 tps = (chunks + W - 1) / W;\n";
+  s << "  const u32 tiles = stripes * tps;\n";
+  s << "  for (u32 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {\n";
+  s << "    const u64 t = tile / tps;\n";
+  s << "    const u32 q = (tile - (u32)t * tps) * W + warp;\n";
   s << "    const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
-  s << "    const bool v0 = o0 < S, v1 = o1 < S;\n";
-  s << "    switch (g) {\n";
-  for (size_t g = 0; g < groups.size(); g++)
-    s << "      case " << g << ": grp" << g << "(R, S, t, o0, o1, v0, v1); break;\n";
-  s << "      default: break;\n    }\n  }\n}\n";
+  s << "    const bool v0 = q < chunks && o0 < S, v1 = q < chunks && o1 < S;\n";
+  for (size_t g = 0; g < groups.size(); g++) s << "    grp" << g << "(R, S, t, o0, o1, v0, v1);\n";
+  s << "  }\n}\n";
   return s.str();
 }
 
@@ -344,7 +346,7 @@ int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides
   if (chunks64 > 0xFFFFFFFFull) { err = "S too large"; return PMRC_EINVAL; }
   const uint32_t chunks = (uint32_t)chunks64;
   // items = stripes * chunks * groups must fit in 32 bits: split launches over stripe ranges
-  const uint64_t per_stripe = (uint64_t)chunks * k.n_groups;
+  const uint64_t per_stripe = (uint64_t)chunks;
   const uint64_t max_stripes = std::max<uint64_t>(1, 0xFFFFFFF0ull / per_stripe);
   std::vector<uint64_t> buf(2 * k.n_slots);
   for (size_t s0 = 0; s0 < stripes; s0 += max_stripes) {
@@ -355,10 +357,10 @@ int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides
     }
     uint64_t S64 = S;
     void *args[] = {buf.data(), &S64, (void *)&ns, (void *)&chunks};
-    const uint64_t items = (uint64_t)ns * per_stripe;
     const uint64_t warps_per_block = k.tpb / 32;
+    const uint64_t tiles = (uint64_t)ns * ((chunks + warps_per_block - 1) / warps_per_block);
     uint64_t grid = (uint64_t)k.sms * k.blocks_per_sm;
-    grid = std::min<uint64_t>(grid, (items + warps_per_block - 1) / warps_per_block);
+    grid = std::min<uint64_t>(grid, tiles);
     grid = std::max<uint64_t>(grid, 1);
     CUresult cr = drv().LaunchKernel((CUfunction)k.function, (unsigned)grid, 1, 1, k.tpb, 1, 1, 0, (CUstream)stream, args,
                                  nullptr);

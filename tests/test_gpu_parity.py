@@ -24,7 +24,6 @@ ENC_CASES = [
     (pm.PMRC_MSR_SPARSE, 4, 8, 1024, 5),
     (pm.PMRC_MBR, 4, 8, 1008, 4),
     (pm.PMRC_MSR_SPARSE, 16, 32, 1024 + 32, 1),
-    (pm.PMRC_MBR, 16, 32, 512, 1),
     (pm.PMRC_MSR_SPARSE, 2, 3, 16, 7),        # smallest code, one vector per block
 ]
 
@@ -208,7 +207,7 @@ def test_repair_project_combine_split_equals_oracle():
     try:
         st.encode()
         for f in (2, 11):
-            H = [i for i in range(n) if i != f][:st.d] if f != 2 else [i for i in range(n) if i not in (2, 0)]
+            H = [i for i in range(n) if i not in (f, 15)]   # omit a Cauchy node: never singular (R10)
             betas = torch.empty((len(H), stripes, S), dtype=torch.uint8, device=DEV)
             for j, h in enumerate(H):
                 pm.pmrc_repair_project(st.code, f, st.piece(h), (betas[j].data_ptr(), S), S, stripes, st.stream)

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
-HOST_SRC = ["gf256.cpp", "construct.cpp", "xorprog.cpp", "plan.cpp", "cudrv.cpp", "capi.cpp"]
+HOST_SRC = ["gf256.cpp", "construct.cpp", "xorprog.cpp", "codegen.cpp", "plan.cpp", "cudrv.cpp", "capi.cpp"]
 LIB = os.path.join(HERE, "libpmrc.so")
 INPUTS_LIB = os.path.join(ROOT, "inputs", "libpmrc_inputs.so")
 NVCC_ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -196,8 +196,13 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         int v = atoi(kv.c_str() + eq + 1);
         if (key == "max_rows" && v > 0) c->gen.max_rows = v;
         if (key == "in_block" && v > 0) c->gen.in_block = v;
-        if (key == "tpb" && v >= 32) c->gen.tpb = v;
+        if (key == "warps" && v >= 1) c->gen.warps = v;
         if (key == "cse") c->gen.cse = v != 0;
+        if (key == "sync_groups") c->gen.sync_groups = v != 0;
+        if (key == "sync_every") c->gen.sync_every = v;
+        if (key == "ld_hint") c->gen.ld_hint = v;
+        if (key == "chunk_loop" && v > 0) c->gen.chunk_loop = v;
+        if (key == "team" && v > 0) c->gen.team = v;
       }
       pos = e + 1;
     }

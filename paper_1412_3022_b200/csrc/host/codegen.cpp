@@ -1,0 +1,557 @@
+// Generator of the bitsliced sm_100a region-linear-combination kernels.
+//
+// Kernel design, driven by what the B200 measurements showed:
+//   * A group = output blocks that read the same inputs (sparse MSR encode: the n-k parity symbols
+//     of one PM symbol index j read the same d inputs).  Its GF(2^8) coefficients, expanded to
+//     8x8 GF(2) matrices with zero coefficients skipped, form one XOR network, shortened by
+//     Paar CSE and emitted as straight-line code: the only coefficient-specific code.
+//   * Work unit = one warp x one 1 KiB chunk (32 lanes x 32 byte positions).  Lane l owns bytes
+//     [16l,16l+16) and [512+16l,512+16l+16) of every block of the chunk.
+//   * Instruction supply is the first-order constraint (profiles/r01): straight-line code that is
+//     not re-executed starves the SM.  So all warps of a CTA execute the same group at the same
+//     time, everything except the XOR networks is a loop, and per-group code stays ~20 KB.
+//   * Memory: each warp runs a 2-stage pipeline: while a stage computes, lane 0 issues TMA 1-D bulk
+//     copies (cp.async.bulk + mbarrier complete_tx) of the next stage's 1 KiB input blocks into the
+//     other shared-memory buffer.  Inputs that a later group reads again keep normal L2 priority;
+//     an input's last read and all parity stores carry an L2 evict-first policy.
+//   * Each lane transposes its 32 bytes per block in place in shared memory (3 delta-swap stages,
+//     LOP3 mux + IMAD shifts) into 8 bit planes; the XOR network reads planes with LDS.128, keeps
+//     the group's 8 x 8 output planes in registers, then transposes back and stores 16-B vectors.
+#include <algorithm>
+#include <map>
+#include <sstream>
+
+#include "plan.hpp"
+
+namespace pmrc {
+
+namespace {
+
+const char *kHeader = R"CUDA(
+typedef unsigned int u32;
+typedef unsigned long long u64;
+// one delta-swap stage of an 8x8 bit transpose (per byte lane):
+//   a' = m ? a : (b << s);  b' = m ? (a >> s) : b   -- LOP3 mux; shifts as IMAD / IMAD.HI (FMA pipe)
+static __device__ __forceinline__ void pm_sw(u32 &a, u32 &b, const int s, const u32 m) {
+  u32 bs, ar, na, nb;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(bs) : "r"(b), "r"(1u << s));
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(ar) : "r"(a), "r"(1u << (32 - s)));
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(na) : "r"(a), "r"(bs), "r"(m));
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(nb) : "r"(ar), "r"(b), "r"(m));
+  a = na;
+  b = nb;
+}
+// 8 words (32 bytes) <-> 8 bit planes (plane b = bit b of the 32 bytes); an involution
+static __device__ __forceinline__ void pm_tr8(u32 &w0, u32 &w1, u32 &w2, u32 &w3, u32 &w4, u32 &w5, u32 &w6, u32 &w7) {
+  pm_sw(w0, w4, 4, 0x0F0F0F0Fu); pm_sw(w1, w5, 4, 0x0F0F0F0Fu); pm_sw(w2, w6, 4, 0x0F0F0F0Fu); pm_sw(w3, w7, 4, 0x0F0F0F0Fu);
+  pm_sw(w0, w2, 2, 0x33333333u); pm_sw(w1, w3, 2, 0x33333333u); pm_sw(w4, w6, 2, 0x33333333u); pm_sw(w5, w7, 2, 0x33333333u);
+  pm_sw(w0, w1, 1, 0x55555555u); pm_sw(w2, w3, 1, 0x55555555u); pm_sw(w4, w5, 1, 0x55555555u); pm_sw(w6, w7, 1, 0x55555555u);
+}
+static __device__ __forceinline__ u32 pm_saddr(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+static __device__ __forceinline__ u64 pm_policy_ef() {
+  u64 p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+static __device__ __forceinline__ void pm_st(unsigned char *p, bool v, u32 a, u32 b, u32 c, u32 d, u64 pol) {
+  if (v) asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;"
+                      :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d), "l"(pol) : "memory");
+}
+static __device__ __forceinline__ uint4 pm_lds(u32 a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+static __device__ __forceinline__ void pm_sts(u32 a, u32 x, u32 y, u32 z, u32 w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+static __device__ __forceinline__ u64 pm_lds64(u32 a) {
+  u64 v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+// 16-B async copy global -> shared with an L2 cache policy; src_size 0 zero-fills (no branch)
+static __device__ __forceinline__ void pm_cp16(u32 dst, const void *src, u32 src_size, u64 pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;"
+               :: "r"(dst), "l"(src), "r"(src_size), "l"(pol) : "memory");
+}
+static __device__ __forceinline__ u64 pm_policy_en() {
+  u64 p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+static __device__ __forceinline__ void pm_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+static __device__ __forceinline__ void pm_cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+static __device__ __forceinline__ void pm_team_sync(u32 id, u32 n) { asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory"); }
+static __device__ __forceinline__ void pm_bar_init(u32 bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar) : "memory");
+}
+static __device__ __forceinline__ void pm_bar_expect(u32 bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+static __device__ __forceinline__ void pm_bar_wait(u32 bar, u32 parity) {
+  u32 ok;
+  do {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+  } while (!ok);
+}
+static __device__ __forceinline__ void pm_bulk(u32 dst, const void *src, u32 bytes, u32 bar, bool ef, u64 pol) {
+  if (ef)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 :: "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+  else
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+)CUDA";
+
+void coef_rows(uint8_t c, uint8_t rows[8]) { gf().bitmatrix(c, rows); }
+
+// Emit an XOR program: base signal i is named base[i]; outputs into outs (assign or accumulate).
+// Statements (temps and output rows) are emitted by a greedy register-pressure-aware list
+// scheduler: among the statements whose temp operands exist, pick the one that minimises
+// (new live values) - (operands that die here), so temps are consumed soon after they are made.
+// need(name) is called before a statement for every base operand it reads (lazy plane loads).
+template <class Need>
+void emit_slp_lazy(std::ostringstream &s, const Slp &p, const std::vector<std::string> &base,
+                   const std::vector<std::string> &outs, bool accumulate, const std::string &tpref, Need need) {
+  const int nin = p.n_in, nt = (int)p.tmp.size(), nr = (int)p.rows.size();
+  const int nst = nt + nr;
+  std::vector<std::vector<int>> ops(nst);
+  for (int i = 0; i < nt; i++) ops[i] = {p.tmp[i][0], p.tmp[i][1]};
+  for (int r = 0; r < nr; r++) ops[nt + r] = p.rows[r];
+  std::vector<int> uses(nin + nt, 0);
+  for (auto &o : ops)
+    for (int x : o) uses[x]++;
+  std::vector<char> done(nst, 0), have(nin + nt, 0), base_live(nin, 0);
+  for (int i = 0; i < nin; i++) have[i] = 1;
+  auto nm = [&](int sig) -> std::string {
+    if (sig < nin) {
+      need(base[sig]);
+      return base[sig];
+    }
+    return tpref + std::to_string(sig - nin);
+  };
+  auto ready = [&](int st) {
+    for (int x : ops[st])
+      if (!have[x]) return false;
+    return true;
+  };
+  for (int step = 0; step < nst; step++) {
+    int best = -1, bestscore = 1 << 30;
+    for (int st = 0; st < nst; st++) {
+      if (done[st] || !ready(st)) continue;
+      int sc = 0;
+      if (st < nt) sc += 1;                                   // defines a temp
+      else if (!accumulate && !ops[st].empty()) sc += 1;      // defines an output (stays live)
+      for (int x : ops[st]) {
+        if (uses[x] == 1) sc -= 1;                            // last use: dies here
+        if (x < nin && !base_live[x]) sc += 1;                // brings a plane in
+      }
+      if (sc < bestscore || (sc == bestscore && st < best)) { bestscore = sc; best = st; }
+    }
+    const int st = best;
+    done[st] = 1;
+    for (int x : ops[st]) {
+      uses[x]--;
+      if (x < nin) base_live[x] = uses[x] > 0;
+    }
+    if (st < nt) {
+      std::string a = nm(ops[st][0]), b = nm(ops[st][1]);
+      s << "    const u32 " << tpref << st << " = " << a << " ^ " << b << ";\n";
+      have[nin + st] = 1;
+    } else {
+      const int r = st - nt;
+      if (ops[st].empty()) {
+        if (!accumulate) s << "    " << outs[r] << " = 0u;\n";
+        continue;
+      }
+      std::vector<std::string> on;
+      for (int x : ops[st]) on.push_back(nm(x));
+      // balanced ternary XOR tree (3-input LOP3 per node): depth log3(k) instead of k/2
+      while (on.size() > 3) {
+        std::vector<std::string> nx;
+        for (size_t j = 0; j < on.size(); j += 3) {
+          if (j + 1 >= on.size()) nx.push_back(on[j]);
+          else if (j + 2 >= on.size()) nx.push_back("(" + on[j] + " ^ " + on[j + 1] + ")");
+          else nx.push_back("(" + on[j] + " ^ " + on[j + 1] + " ^ " + on[j + 2] + ")");
+        }
+        on.swap(nx);
+      }
+      s << "    " << outs[r] << (accumulate ? " ^= " : " = ");
+      for (size_t j = 0; j < on.size(); j++) s << (j ? " ^ " : "") << on[j];
+      s << ";\n";
+    }
+  }
+}
+void emit_slp(std::ostringstream &s, const Slp &p, const std::vector<std::string> &base,
+              const std::vector<std::string> &outs, bool accumulate, const std::string &tpref) {
+  emit_slp_lazy(s, p, base, outs, accumulate, tpref, [](const std::string &) {});
+}
+
+Slp make_slp(int n_in, const std::vector<std::vector<int>> &rows, bool cse) {
+  if (cse) return paar(n_in, rows);
+  Slp s;
+  s.n_in = n_in;
+  s.rows = rows;
+  return s;
+}
+
+struct Group {
+  std::vector<int> rows, cols;
+};
+struct Stage {
+  int g = 0;
+  std::vector<int> cols;  // inputs (plan columns) computed in this stage
+  std::vector<std::pair<int, int>> blocks;  // loaded (slot, blk), in smem slot order
+  std::vector<int> first_block;             // per col: index of its first loaded block
+  std::vector<char> ef;                     // per loaded block: last read -> evict-first
+};
+
+bool is_plain(const InputDesc &in) { return in.terms.size() == 1 && in.terms[0].coef == 1; }
+
+}  // namespace
+
+std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st) {
+  st = GenStats();
+  const int R = (int)p.outputs.size();
+  const int C = (int)p.inputs.size();
+  // ---- groups: output rows with identical support, split into chunks of max_rows ----
+  std::map<std::vector<int>, std::vector<int>> by_support;
+  for (int r = 0; r < R; r++) {
+    std::vector<int> sup;
+    for (int c = 0; c < C; c++)
+      if (p.A.at(r, c)) sup.push_back(c);
+    by_support[sup].push_back(r);
+  }
+  std::vector<Group> groups;
+  for (auto &kv : by_support)
+    for (size_t i = 0; i < kv.second.size(); i += o.max_rows) {
+      Group g;
+      g.cols = kv.first;
+      for (size_t j = i; j < std::min(kv.second.size(), i + (size_t)o.max_rows); j++) g.rows.push_back(kv.second[j]);
+      groups.push_back(g);
+    }
+  st.groups = (int)groups.size();
+
+  // ---- stages: each group's inputs packed into shared-memory buffers of <= IB loaded blocks ----
+  const int IB = std::max(1, o.in_block);
+  std::vector<Stage> stages;
+  std::vector<std::vector<int>> gstages(groups.size());
+  for (size_t g = 0; g < groups.size(); g++) {
+    Stage cur;
+    cur.g = (int)g;
+    for (int c : groups[g].cols) {
+      const InputDesc &in = p.inputs[c];
+      int need = (int)in.terms.size();
+      if (!cur.cols.empty() && (int)cur.blocks.size() + need > IB) {
+        gstages[g].push_back((int)stages.size());
+        stages.push_back(cur);
+        cur = Stage();
+        cur.g = (int)g;
+      }
+      cur.first_block.push_back((int)cur.blocks.size());
+      cur.cols.push_back(c);
+      for (auto &t : in.terms) cur.blocks.push_back({t.slot, t.blk});
+    }
+    if (!cur.cols.empty()) {
+      gstages[g].push_back((int)stages.size());
+      stages.push_back(cur);
+    }
+  }
+  int qmax = 1;
+  for (auto &sg : stages) qmax = std::max(qmax, (int)sg.blocks.size());
+  // L2 policy: a loaded block keeps normal priority if a later stage of the tile loads it again
+  {
+    std::map<std::pair<int, int>, std::pair<int, int>> last;  // block -> (stage, index) of last read
+    for (size_t g = 0; g < groups.size(); g++)
+      for (int si : gstages[g])
+        for (size_t i = 0; i < stages[si].blocks.size(); i++) last[stages[si].blocks[i]] = {si, (int)i};
+    for (size_t si = 0; si < stages.size(); si++) {
+      stages[si].ef.assign(stages[si].blocks.size(), 0);
+      for (size_t i = 0; i < stages[si].blocks.size(); i++) {
+        auto l = last[stages[si].blocks[i]];
+        stages[si].ef[i] = (l.first == (int)si && l.second == (int)i) ? 1 : 0;
+      }
+    }
+  }
+
+  const int M = std::max(1, o.chunk_loop);
+  const int T = std::max(1, o.team);  // warps sharing one chunk's stage buffer
+  std::ostringstream s;
+  s << "// generated by libpmrc (codegen.cpp) — bitsliced GF(2^8) region linear combination\n";
+  s << kHeader;
+  s << "struct Slots { u64 ptr[" << std::max(1, p.n_slots) << "]; u64 stride[" << std::max(1, p.n_slots) << "]; };\n";
+  s << "#define PM_QMAX " << qmax << "u\n";
+  s << "#define PM_T " << T << "u\n";
+  size_t nb_total = 0;
+  for (auto &sg : stages) nb_total += sg.blocks.size();
+  // loaded blocks: (slot << 16 | blk), bit 31 = last read (evict-first)
+  s << "__constant__ u32 pm_blk[" << std::max<size_t>(1, nb_total) << "] = {";
+  {
+    size_t k = 0;
+    for (auto &sg : stages)
+      for (size_t i = 0; i < sg.blocks.size(); i++, k++)
+        s << (k ? ", " : "") << ((sg.ef[i] ? 0x80000000u : 0u) | ((uint32_t)sg.blocks[i].first << 16) |
+                                 (uint32_t)sg.blocks[i].second) << "u";
+    if (!nb_total) s << "0u";
+  }
+  s << "};\n";
+  s << "__constant__ u32 pm_stage_off[" << stages.size() + 1 << "] = {";
+  {
+    size_t off = 0;
+    for (size_t si = 0; si <= stages.size(); si++) {
+      s << (si ? ", " : "") << off << "u";
+      if (si < stages.size()) off += stages[si].blocks.size();
+    }
+  }
+  s << "};\n";
+  std::vector<uint32_t> seq;
+  for (size_t g = 0; g < groups.size(); g++)
+    for (int m = 0; m < M; m++)
+      for (int si : gstages[g]) seq.push_back(((uint32_t)si << 8) | (uint32_t)m);
+  const size_t L = seq.size();
+  s << "#define PM_L " << L << "u\n";
+  s << "__constant__ u32 pm_seq[" << std::max<size_t>(1, L) << "] = {";
+  for (size_t i = 0; i < L; i++) s << (i ? ", " : "") << seq[i] << "u";
+  if (!L) s << "0u";
+  s << "};\n";
+
+  s << R"CUDA(
+// in-place 8x8 bit transpose of this lane's 32 bytes of blocks [lo, hi) of a stage buffer
+static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 lo, const u32 hi) {
+  #pragma unroll 1
+  for (u32 i = lo; i < hi; i++) {
+    const u32 a0 = buf + i * 1024u, a1 = a0 + 512u;
+    const uint4 a = pm_lds(a0), b = pm_lds(a1);
+    u32 w0 = a.x, w1 = a.y, w2 = a.z, w3 = a.w, w4 = b.x, w5 = b.y, w6 = b.z, w7 = b.w;
+    pm_tr8(w0, w1, w2, w3, w4, w5, w6, w7);
+    pm_sts(a0, w0, w1, w2, w3);
+    pm_sts(a1, w4, w5, w6, w7);
+  }
+}
+)CUDA";
+
+  static const char *comp[4] = {"x", "y", "z", "w"};
+  // ---- prefetch code for a stage (static block list; runtime stripe tt, chunk qq, buffer bb) ----
+  auto emit_issue = [&](std::ostringstream &o2, int sid, const std::string &tt, const std::string &qq,
+                        const std::string &bb, const std::string &ind) {
+    const Stage &sg = stages[sid];
+    const int n = (int)sg.blocks.size();
+    o2 << ind << "{ const u64 qo = (u64)(" << qq << ") * 1024u + lane * 16u;\n";
+    o2 << ind << "  const bool okq = (" << qq << ") < chunks;\n";
+    o2 << ind << "  const u32 z0 = (okq && qo < S) ? 16u : 0u, z1 = (okq && qo + 512u < S) ? 16u : 0u;\n";
+    o2 << ind << "  const u32 dst = sbuf + (" << bb << ") * (PM_QMAX * 1024u) + lane * 16u;\n";
+    o2 << ind << "  switch (rank) {\n";
+    for (int rk = 0; rk < T; rk++) {
+      const int lo = n * rk / T, hi = n * (rk + 1) / T;
+      o2 << ind << "  case " << rk << ": {\n";
+      std::map<int, bool> slots;
+      for (int i = lo; i < hi; i++) slots[sg.blocks[i].first] = true;
+      for (auto &kv : slots)
+        o2 << ind << "    const u64 sb" << kv.first << " = R.ptr[" << kv.first << "] + (" << tt << ") * R.stride["
+           << kv.first << "] + qo;\n";
+      for (int i = lo; i < hi; i++) {
+        const auto &bk = sg.blocks[i];
+        o2 << ind << "    { const u64 a = sb" << bk.first << " + (u64)" << bk.second << "u * S;\n";
+        o2 << ind << "      pm_cp16(dst + " << i * 1024 << "u, (const void *)(z0 ? a : sb" << bk.first << "), z0, "
+           << (sg.ef[i] ? "pol_ef" : "pol_en") << ");\n";
+        o2 << ind << "      pm_cp16(dst + " << i * 1024 + 512 << "u, (const void *)(z1 ? a + 512u : sb" << bk.first
+           << "), z1, " << (sg.ef[i] ? "pol_ef" : "pol_en") << "); }\n";
+      }
+      o2 << ind << "  } break;\n";
+    }
+    o2 << ind << "  default: break;\n" << ind << "  }\n" << ind << "}\n";
+  };
+
+  const int TPB = 32 * std::max(T, o.warps);
+  const int teams = TPB / 32 / T;
+  s << "extern \"C\" __global__ void __launch_bounds__(" << TPB << ", 1) pmrc_kernel(const __grid_constant__ Slots R, "
+       "const u64 S, const u32 stripes, const u32 chunks) {\n";
+  s << "  extern __shared__ __align__(1024) unsigned char pm_smem[];\n";
+  s << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, team = warp / PM_T, rank = warp - team * PM_T;\n";
+  s << "  const u32 per = " << teams << "u * " << M << "u;\n";
+  s << "  const u32 tps = (chunks + per - 1u) / per;\n";
+  s << "  const u32 tiles = stripes * tps;\n";
+  s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (2u * PM_QMAX * 1024u);\n";
+  s << "  const u32 lbuf = sbuf + lane * 16u;\n";
+  s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en();\n";
+  s << "  u32 pb = 0u;\n";
+  // first prefetch: first stage of the first tile
+  int first_sid = -1;
+  for (size_t g = 0; g < groups.size() && first_sid < 0; g++)
+    if (!gstages[g].empty()) first_sid = gstages[g][0];
+  if (first_sid >= 0) {
+    s << "  if (blockIdx.x < tiles) {\n";
+    s << "    const u64 t0 = blockIdx.x / tps;\n";
+    s << "    const u32 q0 = (blockIdx.x - (u32)t0 * tps) * per + team * " << M << "u;\n";
+    emit_issue(s, first_sid, "t0", "q0", "0u", "    ");
+    s << "  }\n";
+  }
+  s << "  pm_cp_commit();\n";
+  s << "  for (u32 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {\n";
+  s << "    const u64 t = tile / tps;\n";
+  s << "    const u32 qb = (tile - (u32)t * tps) * per + team * " << M << "u;\n";
+  s << "    const u32 ntile = tile + gridDim.x;\n";
+  s << "    const u64 tn = ntile / tps;\n";
+  s << "    const u32 qn = (ntile - (u32)tn * tps) * per + team * " << M << "u;\n";
+  for (size_t g = 0; g < groups.size(); g++) {
+    const Group &G = groups[g];
+    const int mall = (int)G.rows.size();
+    // successor group with stages (for the prefetch after this group's last stage at m = M-1)
+    int next_g = -1;
+    for (size_t g2 = g + 1; g2 < groups.size(); g2++)
+      if (!gstages[g2].empty()) { next_g = (int)g2; break; }
+    if (o.sync_groups) s << "    __syncthreads();\n";
+    s << "    #pragma unroll 1\n";
+    s << "    for (u32 m = 0; m < " << M << "u; m++) {\n";
+    s << "      const u32 q = qb + m;\n";
+    s << "      const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
+    s << "      const bool v0 = q < chunks && o0 < S, v1 = q < chunks && o1 < S;\n";
+    s << "      switch (rank) {\n";
+    for (int rk = 0; rk < T; rk++) {
+      const int r0 = mall * rk / T, r1 = mall * (rk + 1) / T;
+      const int m = r1 - r0;
+      s << "      case " << rk << ": {\n";
+      std::vector<std::string> outs;
+      for (int r = 0; r < m; r++)
+        for (int b = 0; b < 8; b++) outs.push_back("o" + std::to_string(r) + "_" + std::to_string(b));
+      if (!outs.empty()) {
+        s << "        u32 ";
+        for (size_t i = 0; i < outs.size(); i++) s << (i ? ", " : "") << outs[i];
+        s << ";\n";
+      }
+      if (gstages[g].empty())
+        for (auto &nn : outs) s << "        " << nn << " = 0u;\n";
+      bool first = true;
+      for (size_t sj = 0; sj < gstages[g].size(); sj++) {
+        const int si = gstages[g][sj];
+        const Stage &sg = stages[si];
+        const int nblk = (int)sg.blocks.size();
+        s << "        {\n";
+        // consume: own copies landed -> transpose own share -> team barrier
+        s << "          pm_cp_wait0();\n";
+        s << "          const u32 buf = sbuf + pb * (PM_QMAX * 1024u);\n";
+        s << "          pm_transpose_in(buf + lane * 16u, " << nblk * rk / T << "u, " << nblk * (rk + 1) / T << "u);\n";
+        s << "          " << (T > 1 ? "pm_team_sync(1u + team, PM_T * 32u);" : "__syncwarp();") << "\n";
+        // prefetch the successor stage into the other buffer
+        if (sj + 1 < gstages[g].size()) {
+          emit_issue(s, gstages[g][sj + 1], "t", "q", "pb ^ 1u", "          ");
+        } else {
+          s << "          if (m + 1u < " << M << "u) {\n";
+          emit_issue(s, gstages[g][0], "t", "q + 1u", "pb ^ 1u", "            ");
+          s << "          } else {\n";
+          if (next_g >= 0) {
+            emit_issue(s, gstages[next_g][0], "t", "qb", "pb ^ 1u", "            ");
+          } else if (first_sid >= 0) {
+            s << "            if (ntile < tiles) {\n";
+            emit_issue(s, first_sid, "tn", "qn", "pb ^ 1u", "              ");
+            s << "            }\n";
+          }
+          s << "          }\n";
+        }
+        s << "          pm_cp_commit();\n";
+        s << "          const u32 pl = buf + lane * 16u;\n";
+        if (m > 0) {
+          std::vector<std::string> base;
+          std::vector<char> used_half(2 * nblk, 0);
+          std::ostringstream body;
+          for (size_t ci = 0; ci < sg.cols.size(); ci++) {
+            const InputDesc &in = p.inputs[sg.cols[ci]];
+            const int fb = sg.first_block[ci];
+            if (is_plain(in)) {
+              for (int b = 0; b < 8; b++) base.push_back("P" + std::to_string(2 * fb + b / 4) + "." + comp[b % 4]);
+              continue;
+            }
+            std::string nm = "d" + std::to_string(ci);
+            std::vector<std::string> dbase;
+            std::vector<std::vector<int>> drows(8);
+            for (size_t u = 0; u < in.terms.size(); u++) {
+              const int bi = fb + (int)u;
+              uint8_t br[8];
+              coef_rows(in.terms[u].coef, br);
+              for (int bb = 0; bb < 8; bb++) {
+                dbase.push_back("P" + std::to_string(2 * bi + bb / 4) + "." + comp[bb % 4]);
+                for (int bp = 0; bp < 8; bp++)
+                  if ((br[bb] >> bp) & 1) drows[bb].push_back((int)u * 8 + bp);
+              }
+            }
+            Slp ds = make_slp((int)dbase.size(), drows, o.cse);
+            if (rk == 0) {
+              st.xor2 += ds.xor2();
+              st.naive_lop3 += naive_lop3(drows);
+              st.xor2_naive += make_slp((int)dbase.size(), drows, false).xor2();
+            }
+            body << "          u32 " << nm << "_0, " << nm << "_1, " << nm << "_2, " << nm << "_3, " << nm << "_4, " << nm
+                 << "_5, " << nm << "_6, " << nm << "_7;\n";
+            std::vector<std::string> dout;
+            for (int bb = 0; bb < 8; bb++) dout.push_back(nm + "_" + std::to_string(bb));
+            emit_slp(body, ds, dbase, dout, false, nm + "t");
+            for (size_t u = 0; u < in.terms.size(); u++) used_half[2 * (fb + u)] = used_half[2 * (fb + u) + 1] = 1;
+            for (int b = 0; b < 8; b++) base.push_back(nm + "_" + std::to_string(b));
+          }
+          std::vector<std::vector<int>> rows(8 * m);
+          for (int r = 0; r < m; r++)
+            for (size_t ci = 0; ci < sg.cols.size(); ci++) {
+              uint8_t cf = p.A.at(G.rows[r0 + r], sg.cols[ci]);
+              if (!cf) continue;
+              uint8_t br[8];
+              coef_rows(cf, br);
+              for (int b = 0; b < 8; b++)
+                for (int bp = 0; bp < 8; bp++)
+                  if ((br[b] >> bp) & 1) rows[r * 8 + b].push_back((int)ci * 8 + bp);
+            }
+          Slp sl = make_slp((int)base.size(), rows, o.cse);
+          st.xor2 += sl.xor2() + (first ? 0 : 8 * m);
+          st.naive_lop3 += naive_lop3(rows);
+          st.xor2_naive += make_slp((int)base.size(), rows, false).xor2() + (first ? 0 : 8 * m);
+          std::vector<char> loaded(2 * nblk, 0);
+          std::ostringstream net;
+          auto need = [&](const std::string &nmb) {
+            if (nmb[0] != 'P') return;
+            int h = std::stoi(nmb.substr(1, nmb.find('.') - 1));
+            if (loaded[h]) return;
+            loaded[h] = 1;
+            net << "          const uint4 P" << h << " = pm_lds(pl + " << (h / 2) * 1024 + (h % 2) * 512 << "u);\n";
+          };
+          for (int h = 0; h < 2 * nblk; h++)
+            if (used_half[h] && !loaded[h]) need("P" + std::to_string(h) + ".x");
+          net << body.str();
+          emit_slp_lazy(net, sl, base, outs, !first, "t", need);
+          s << net.str();
+          first = false;
+        }
+        s << "          pb ^= 1u;\n";
+        s << "        }\n";
+        if (rk == 0) {
+          st.loads += nblk;
+          st.transposes += nblk;
+        }
+      }
+      // transpose back and store (evict-first: parity is not re-read)
+      std::map<int, bool> oslots;
+      for (int r = 0; r < m; r++) oslots[p.outputs[G.rows[r0 + r]].slot] = true;
+      for (auto &kv : oslots)
+        s << "        const u64 ob" << kv.first << " = R.ptr[" << kv.first << "] + t * R.stride[" << kv.first << "];\n";
+      for (int r = 0; r < m; r++) {
+        const OutputDesc &od = p.outputs[G.rows[r0 + r]];
+        std::string n = "o" + std::to_string(r);
+        s << "        pm_tr8(" << n << "_0, " << n << "_1, " << n << "_2, " << n << "_3, " << n << "_4, " << n << "_5, "
+          << n << "_6, " << n << "_7);\n";
+        s << "        { unsigned char *pp = (unsigned char *)(ob" << od.slot << " + (u64)" << od.blk << "u * S);\n";
+        s << "          pm_st(pp + o0, v0, " << n << "_0, " << n << "_1, " << n << "_2, " << n << "_3, pol_ef);\n";
+        s << "          pm_st(pp + o1, v1, " << n << "_4, " << n << "_5, " << n << "_6, " << n << "_7, pol_ef); }\n";
+        if (rk == 0) st.transposes++;
+      }
+      s << "      } break;\n";
+    }
+    s << "      default: break;\n      }\n";
+    s << "    }\n";
+  }
+  s << "  }\n}\n";
+  st.smem_per_warp = (2 * qmax * 1024 + T - 1) / T;
+  return s.str();
+}
+
+}  // namespace pmrc

@@ -14,12 +14,13 @@ const Drv &drv() {
     PM_SYM(ModuleUnload, "cuModuleUnload");
     PM_SYM(ModuleGetFunction, "cuModuleGetFunction");
     PM_SYM(FuncGetAttribute, "cuFuncGetAttribute");
+    PM_SYM(FuncSetAttribute, "cuFuncSetAttribute");
     PM_SYM(OccupancyMaxActiveBlocksPerMultiprocessor, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
     PM_SYM(CtxGetDevice, "cuCtxGetDevice");
     PM_SYM(DeviceGetAttribute, "cuDeviceGetAttribute");
     PM_SYM(LaunchKernel, "cuLaunchKernel");
 #undef PM_SYM
-    x.ok = x.GetErrorString && x.ModuleLoadData && x.ModuleUnload && x.ModuleGetFunction && x.FuncGetAttribute &&
+    x.ok = x.GetErrorString && x.ModuleLoadData && x.ModuleUnload && x.ModuleGetFunction && x.FuncGetAttribute && x.FuncSetAttribute &&
            x.OccupancyMaxActiveBlocksPerMultiprocessor && x.CtxGetDevice && x.DeviceGetAttribute && x.LaunchKernel;
     return x;
   }();

@@ -12,6 +12,7 @@ struct Drv {
   CUresult (*ModuleUnload)(CUmodule) = nullptr;
   CUresult (*ModuleGetFunction)(CUfunction *, CUmodule, const char *) = nullptr;
   CUresult (*FuncGetAttribute)(int *, CUfunction_attribute, CUfunction) = nullptr;
+  CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
   CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int *, CUfunction, int, size_t) = nullptr;
   CUresult (*CtxGetDevice)(CUdevice *) = nullptr;
   CUresult (*DeviceGetAttribute)(int *, CUdevice_attribute, CUdevice) = nullptr;

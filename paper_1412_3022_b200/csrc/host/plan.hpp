@@ -37,9 +37,15 @@ struct PlanSpec {
 
 struct GenOptions {
   int max_rows = 8;      // output blocks per group (8 planes each in registers)
-  int in_block = 16;     // inputs per CSE block (register pressure vs. sharing)
-  int tpb = 256;         // threads per CTA
+  int in_block = 14;     // loaded blocks per stage (shared-memory buffer of in_block KiB, x2)
+  int warps = 8;         // warps per CTA (capped by the 220 KiB shared-memory budget)
+  int tpb = 256;         // (derived) threads per CTA
   bool cse = true;       // Paar CSE (false: naive per-row XOR chains)
+  bool sync_groups = true;  // __syncthreads() before each group: warps of a CTA execute the same code
+  int sync_every = 0;       // also sync every N emitted XOR statements (0 = off)
+  int chunk_loop = 8;       // chunks per team per group (loop: instruction reuse)
+  int team = 2;             // warps sharing one chunk's stage buffer (each computes 1/team of the rows)
+  int ld_hint = 1;          // 0: __ldg/__stcs; 1: L2 evict-first cache-hinted loads/stores
 };
 
 struct GenStats {
@@ -49,6 +55,7 @@ struct GenStats {
   long xor2_naive = 0;   // 2-input XORs without CSE
   int transposes = 0;    // 8x8 bit transposes per 32 byte positions (in + out)
   long loads = 0;        // 16-B vector loads per lane per item sum
+  int smem_per_warp = 0; // bytes of shared memory (transposed input planes) per warp
 };
 
 // Generate CUDA C++ source of the bitsliced kernel `pmrc_kernel` for a plan.
@@ -61,6 +68,8 @@ struct Kernel {
   int n_slots = 0;
   int n_groups = 0;
   int tpb = 256;
+  int chunk_loop = 1;
+  size_t smem = 0;
   int blocks_per_sm = 1;
   int sms = 148;
   int regs = 0;

@@ -17,6 +17,17 @@ int main(int argc, char **argv) {
   for (int r = 0; r < c.P; r++) p.outputs.push_back({1, r});
   p.A = c.Gpp;
   GenOptions o; o.max_rows = mr; o.in_block = ib; o.cse = cse;
+  if (argc > 7) {  // key=value,... (team, warps, chunk_loop)
+    std::string g = argv[7]; size_t pos = 0;
+    while (pos < g.size()) {
+      size_t e = g.find(',', pos); if (e == std::string::npos) e = g.size();
+      std::string kv = g.substr(pos, e - pos); size_t eq = kv.find('=');
+      if (eq != std::string::npos) { std::string k = kv.substr(0, eq); int v = atoi(kv.c_str() + eq + 1);
+        if (k == "team") o.team = v; if (k == "warps") o.warps = v; if (k == "chunk_loop") o.chunk_loop = v; }
+      pos = e + 1;
+    }
+  }
+  if (o.warps == 0) o.warps = 16;
   GenStats st;
   std::string src = generate_source(p, o, st);
   long nnz = 0; for (auto v : c.Gpp.a) nnz += v != 0;

@@ -355,10 +355,11 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
       for (int i = lo; i < hi; i++) {
         const auto &bk = sg.blocks[i];
         o2 << ind << "    { const u64 a = sb" << bk.first << " + (u64)" << bk.second << "u * S;\n";
-        o2 << ind << "      pm_cp16(dst + " << i * 1024 << "u, (const void *)(z0 ? a : sb" << bk.first << "), z0, "
-           << (sg.ef[i] ? "pol_ef" : "pol_en") << ");\n";
-        o2 << ind << "      pm_cp16(dst + " << i * 1024 + 512 << "u, (const void *)(z1 ? a + 512u : sb" << bk.first
-           << "), z1, " << (sg.ef[i] ? "pol_ef" : "pol_en") << "); }\n";
+        // src_size 0 (chunk beyond S) zero-fills without reading the source
+        o2 << ind << "      pm_cp16(dst + " << i * 1024 << "u, (const void *)a, z0, " << (sg.ef[i] ? "pol_ef" : "pol_en")
+           << ");\n";
+        o2 << ind << "      pm_cp16(dst + " << i * 1024 + 512 << "u, (const void *)(a + 512u), z1, "
+           << (sg.ef[i] ? "pol_ef" : "pol_en") << "); }\n";
       }
       o2 << ind << "  } break;\n";
     }

@@ -151,7 +151,7 @@ def main():
     import inputs
     import paper_1412_3022_b200 as pm
     from paper_1412_3022_b200 import build as pmbuild
-    pmbuild.build_all()
+    pmbuild.build_all(kernels=False)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

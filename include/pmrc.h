@@ -139,6 +139,15 @@ int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids, int n_
  * P:209), nnz(psi_f) for MBR, 1 for RS. */
 int pmrc_read_cost(const pmrc_code *c, int lost_id, int *blocks_per_helper);
 
+/* Generate the encode kernel and NVRTC-compile it (sm_100a) into the in-tree kernel cache
+ * (paper_1412_3022_b200/kcache, or $PMRC_KCACHE) without loading it: needs no GPU.  build() uses it
+ * so that pmrc_create on the GPU box loads a cached cubin instead of compiling. */
+int pmrc_precompile(const pmrc_code *c);
+
+/* The generated CUDA source of the encode kernel (for inspection / offline nvcc builds).  Writes
+ * up to cap bytes (NUL-terminated if room) and the full length to *len. */
+int pmrc_encode_source(const pmrc_code *c, char *buf, size_t cap, size_t *len);
+
 /* Number of kernels this library launched since load (for the bench's gpu_launches claim). */
 unsigned long long pmrc_launch_count(void);
 

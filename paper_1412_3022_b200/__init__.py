@@ -20,7 +20,8 @@ MATRIX_PSI, MATRIX_G, MATRIX_GSYS, MATRIX_GPP, MATRIX_LAMBDA = 0, 1, 2, 3, 4
 
 EXPORTS = ["pmrc_create", "pmrc_destroy", "pmrc_info", "pmrc_matrix", "pmrc_layout", "pmrc_encode",
            "pmrc_encode_host", "pmrc_decode", "pmrc_repair", "pmrc_repair_project", "pmrc_repair_combine",
-           "pmrc_read_cost", "pmrc_launch_count", "pmrc_strerror", "pmrc_last_error"]
+           "pmrc_read_cost", "pmrc_launch_count", "pmrc_strerror", "pmrc_last_error", "pmrc_precompile",
+           "pmrc_encode_source"]
 
 
 class PmrcError(RuntimeError):
@@ -73,6 +74,8 @@ def lib():
             "pmrc_repair_combine": ([P, I, IP, I, ctypes.POINTER(pmrc_cregion), pmrc_region, Z, Z, P], I),
             "pmrc_read_cost": ([P, I, IP], I),
             "pmrc_launch_count": ([], ctypes.c_ulonglong),
+            "pmrc_precompile": ([P], I),
+            "pmrc_encode_source": ([P, P, Z, ctypes.POINTER(ctypes.c_size_t)], I),
             "pmrc_strerror": ([I], ctypes.c_char_p),
             "pmrc_last_error": ([], ctypes.c_char_p),
         }
@@ -175,6 +178,18 @@ def pmrc_read_cost(code, lost_id):
     b = ctypes.c_int()
     _check(lib().pmrc_read_cost(code, lost_id, ctypes.byref(b)), "pmrc_read_cost")
     return b.value
+
+
+def pmrc_precompile(code):
+    _check(lib().pmrc_precompile(code), "pmrc_precompile")
+
+
+def pmrc_encode_source(code):
+    n = ctypes.c_size_t()
+    _check(lib().pmrc_encode_source(code, None, 0, ctypes.byref(n)), "pmrc_encode_source")
+    buf = ctypes.create_string_buffer(n.value + 1)
+    _check(lib().pmrc_encode_source(code, buf, n.value + 1, ctypes.byref(n)), "pmrc_encode_source")
+    return buf.value.decode()
 
 
 def pmrc_launch_count():

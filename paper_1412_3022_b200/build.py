@@ -53,9 +53,40 @@ def build_inputs(force=False):
     return INPUTS_LIB
 
 
-def build_all(force=False):
+# encode plans pre-compiled (NVRTC, sm_100a) into the in-tree kernel cache by build(): the bench
+# configuration and the GPU-test shapes.  (kind, k, d, n)
+PRECOMPILE = [(0, 8, 14, 16), (0, 3, 4, 6), (2, 8, 14, 16), (3, 8, 8, 16), (0, 8, 14, 15), (1, 8, 14, 16),
+              (0, 4, 6, 8), (2, 4, 6, 8), (0, 2, 2, 3), (1, 3, 4, 6), (2, 3, 4, 6), (3, 3, 3, 6), (0, 16, 30, 32)]
+
+
+def _precompile_one(args):
+    import ctypes
+    L = ctypes.CDLL(LIB)
+    h = ctypes.c_void_p()
+    kind, k, d, n = args
+    rc = L.pmrc_create(ctypes.byref(h), kind, k, d, n, 8)
+    if rc == 0:
+        rc = L.pmrc_precompile(h)
+        L.pmrc_destroy(h)
+    return args, rc
+
+
+def precompile(configs=PRECOMPILE):
+    """NVRTC-compile the encode kernels of `configs` into paper_1412_3022_b200/kcache (no GPU)."""
+    from multiprocessing import get_context
+    with get_context("spawn").Pool(min(len(configs), os.cpu_count() or 4)) as pool:
+        res = pool.map(_precompile_one, configs)
+    bad = [r for r in res if r[1] != 0]
+    if bad:
+        raise RuntimeError("precompile failed: %s" % bad)
+    return res
+
+
+def build_all(force=False, kernels=True):
     build_inputs(force)
     build_lib(force)
+    if kernels:
+        precompile()
 
 
 if __name__ == "__main__":

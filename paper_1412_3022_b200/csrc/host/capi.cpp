@@ -262,6 +262,27 @@ int pmrc_info(const pmrc_code *c, pmrc_info_t *o) {
   return PMRC_OK;
 }
 
+int pmrc_precompile(const pmrc_code *c) {
+  if (!c) return fail(PMRC_EINVAL, "NULL handle");
+  std::string err;
+  int rc = precompile_kernel(c->enc_spec, c->gen, err);
+  if (rc) return fail(rc, err);
+  return PMRC_OK;
+}
+
+int pmrc_encode_source(const pmrc_code *c, char *buf, size_t cap, size_t *len) {
+  if (!c) return fail(PMRC_EINVAL, "NULL handle");
+  GenStats st;
+  std::string src = generate_source(c->enc_spec, c->gen, st);
+  if (len) *len = src.size();
+  if (buf && cap) {
+    size_t n = std::min(cap - 1, src.size());
+    memcpy(buf, src.data(), n);
+    buf[n] = 0;
+  }
+  return PMRC_OK;
+}
+
 int pmrc_matrix(const pmrc_code *c, int which, uint8_t *buf, int *rows, int *cols) {
   if (!c || !rows || !cols) return fail(PMRC_EINVAL, "NULL argument");
   const CodeDef &D = c->def;

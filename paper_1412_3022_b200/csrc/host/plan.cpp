@@ -5,8 +5,13 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <dlfcn.h>
+#include <sys/stat.h>
+
 #include <algorithm>
+#include <fstream>
 #include <chrono>
+#include <unistd.h>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -30,29 +35,59 @@ std::string cu_err(CUresult r) {
 }
 }  // namespace
 
-int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string &err) {
-  auto t0 = std::chrono::steady_clock::now();
-  k = Kernel();
-  GenOptions oo = o;
-  {
-    // warps per CTA from the shared-memory budget (2 stage buffers of in_block KiB per warp)
-    GenStats probe;
-    (void)generate_source(p, oo, probe);  // cheap relative to NVRTC; gives smem_per_warp
-    int budget = 220 * 1024;
-    int w = std::max(1, std::min(16, budget / std::max(1, probe.smem_per_warp)));
-    if (o.warps > 0) w = std::min(w, o.warps);
-    w = std::max(oo.team, w - w % std::max(1, oo.team));  // whole teams
-    oo.warps = w;
+// Compiled-kernel cache: cubins keyed by a hash of the generated source, stored in-tree next to
+// libpmrc.so (kcache/) so build() can pre-compile the standard plans on a machine without a GPU
+// and the GPU box loads them without NVRTC.  PMRC_KCACHE overrides the directory; "off" disables.
+static std::string cache_dir() {
+  if (const char *e = getenv("PMRC_KCACHE")) return std::string(e) == "off" ? "" : std::string(e);
+  Dl_info info;
+  if (dladdr((void *)&cache_dir, &info) && info.dli_fname) {
+    std::string so = info.dli_fname;
+    size_t sl = so.rfind('/');
+    return (sl == std::string::npos ? std::string(".") : so.substr(0, sl)) + "/kcache";
   }
+  return "";
+}
+
+static std::string source_key(const std::string &src) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char ch : src) h = (h ^ ch) * 1099511628211ull;
+  char buf[64];
+  snprintf(buf, sizeof buf, "%016llx_%zu", (unsigned long long)h, src.size());
+  return buf;
+}
+
+static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
+  GenOptions oo = o;
+  // warps per CTA from the shared-memory budget (2 stage buffers of in_block KiB per team)
+  GenStats probe;
+  (void)generate_source(p, oo, probe);
+  int budget = 220 * 1024;
+  int w = std::max(1, std::min(16, budget / std::max(1, probe.smem_per_warp)));
+  if (o.warps > 0) w = std::min(w, o.warps);
+  w = std::max(oo.team, w - w % std::max(1, oo.team));  // whole teams
+  oo.warps = w;
   oo.tpb = 32 * oo.warps;
-  k.source = generate_source(p, oo, k.stats);
-  k.n_slots = std::max(1, p.n_slots);
-  k.n_groups = std::max(1, k.stats.groups);
-  k.tpb = oo.tpb;
-  k.chunk_loop = oo.chunk_loop;
-  k.smem = (size_t)k.stats.smem_per_warp * oo.warps;
+  return oo;
+}
+
+// NVRTC compile (no GPU needed) with the on-disk cache; returns the cubin.
+static int compile_cubin(const std::string &src, std::vector<char> &cubin, bool &from_cache, std::string &err) {
+  from_cache = false;
+  const std::string dir = cache_dir();
+  const std::string path = dir.empty() ? "" : dir + "/" + source_key(src) + ".cubin";
+  if (!path.empty()) {
+    std::ifstream f(path, std::ios::binary);
+    if (f) {
+      cubin.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+      if (!cubin.empty()) {
+        from_cache = true;
+        return PMRC_OK;
+      }
+    }
+  }
   nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, k.source.c_str(), "pmrc_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+  if (nvrtcCreateProgram(&prog, src.c_str(), "pmrc_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     err = "nvrtcCreateProgram failed";
     return PMRC_EJIT;
   }
@@ -69,11 +104,49 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
   }
   size_t nc = 0;
   nvrtcGetCUBINSize(prog, &nc);
-  std::vector<char> cubin(nc);
+  cubin.resize(nc);
   nvrtcGetCUBIN(prog, cubin.data());
   nvrtcDestroyProgram(&prog);
+  if (!path.empty()) {
+    mkdir(dir.c_str(), 0755);
+    std::string tmp = path + ".tmp" + std::to_string((long)getpid());
+    std::ofstream f(tmp, std::ios::binary);
+    if (f.write(cubin.data(), (std::streamsize)cubin.size())) {
+      f.close();
+      rename(tmp.c_str(), path.c_str());
+    } else {
+      remove(tmp.c_str());
+    }
+  }
+  return PMRC_OK;
+}
+
+int precompile_kernel(const PlanSpec &p, const GenOptions &o, std::string &err) {
+  GenOptions oo = resolve_options(p, o);
+  GenStats st;
+  std::string src = generate_source(p, oo, st);
+  std::vector<char> cubin;
+  bool cached = false;
+  return compile_cubin(src, cubin, cached, err);
+}
+
+int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string &err) {
+  auto t0 = std::chrono::steady_clock::now();
+  k = Kernel();
+  GenOptions oo = resolve_options(p, o);
+  k.source = generate_source(p, oo, k.stats);
+  k.n_slots = std::max(1, p.n_slots);
+  k.n_groups = std::max(1, k.stats.groups);
+  k.tpb = oo.tpb;
+  k.chunk_loop = oo.chunk_loop;
+  k.smem = (size_t)k.stats.smem_per_warp * oo.warps;
+  std::vector<char> cubin;
+  bool cached = false;
+  int crc = compile_cubin(k.source, cubin, cached, err);
+  if (crc) return crc;
   auto t1 = std::chrono::steady_clock::now();
   k.compile_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  k.from_cache = cached;
 
   // load into the current context (the runtime's primary context for the current device)
   if (cudaFree(0) != cudaSuccess) {

@@ -76,11 +76,14 @@ struct Kernel {
   GenStats stats;
   std::string source;
   double compile_ms = 0;
+  bool from_cache = false;
 };
 
 // Generate + NVRTC-compile + load.  Returns 0 or PMRC_E*; err gets the log on failure.
 int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string &err);
 void free_kernel(Kernel &k);
+// Generate + NVRTC-compile into the kernel cache only (no GPU needed).
+int precompile_kernel(const PlanSpec &p, const GenOptions &o, std::string &err);
 
 // Launch over `stripes` stripes of S-byte blocks.  ptrs/strides: n_slots entries.
 int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides, size_t S, size_t stripes,

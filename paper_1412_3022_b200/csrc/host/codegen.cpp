@@ -335,12 +335,14 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
 
   static const char *comp[4] = {"x", "y", "z", "w"};
   // ---- prefetch code for a stage (static block list; runtime stripe tt, chunk qq, buffer bb) ----
-  auto emit_issue = [&](std::ostringstream &o2, int sid, const std::string &tt, const std::string &qq,
+  auto emit_issue = [&](std::ostringstream &o2, int sid, const std::string &gi, const std::string &valid,
                         const std::string &bb, const std::string &ind) {
     const Stage &sg = stages[sid];
     const int n = (int)sg.blocks.size();
-    o2 << ind << "{ const u64 qo = (u64)(" << qq << ") * 1024u + lane * 16u;\n";
-    o2 << ind << "  const bool okq = (" << qq << ") < chunks;\n";
+    o2 << ind << "{ const u32 gq = " << gi << ";\n";
+    o2 << ind << "  const u64 tt = gq / chunks;\n";
+    o2 << ind << "  const u64 qo = (u64)(gq - (u32)tt * chunks) * 1024u + lane * 16u;\n";
+    o2 << ind << "  const bool okq = " << valid << ";\n";
     o2 << ind << "  const u32 z0 = (okq && qo < S) ? 16u : 0u, z1 = (okq && qo + 512u < S) ? 16u : 0u;\n";
     o2 << ind << "  const u32 dst = sbuf + (" << bb << ") * (PM_QMAX * 1024u) + lane * 16u;\n";
     o2 << ind << "  switch (rank) {\n";
@@ -350,8 +352,8 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
       std::map<int, bool> slots;
       for (int i = lo; i < hi; i++) slots[sg.blocks[i].first] = true;
       for (auto &kv : slots)
-        o2 << ind << "    const u64 sb" << kv.first << " = R.ptr[" << kv.first << "] + (" << tt << ") * R.stride["
-           << kv.first << "] + qo;\n";
+        o2 << ind << "    const u64 sb" << kv.first << " = R.ptr[" << kv.first << "] + tt * R.stride[" << kv.first
+           << "] + qo;\n";
       for (int i = lo; i < hi; i++) {
         const auto &bk = sg.blocks[i];
         o2 << ind << "    { const u64 a = sb" << bk.first << " + (u64)" << bk.second << "u * S;\n";
@@ -372,31 +374,32 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
        "const u64 S, const u32 stripes, const u32 chunks) {\n";
   s << "  extern __shared__ __align__(1024) unsigned char pm_smem[];\n";
   s << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, team = warp / PM_T, rank = warp - team * PM_T;\n";
-  s << "  const u32 per = " << teams << "u * " << M << "u;\n";
-  s << "  const u32 tps = (chunks + per - 1u) / per;\n";
-  s << "  const u32 tiles = stripes * tps;\n";
+  // Work distribution: CTA b owns the contiguous global chunk range [c0, c1) (chunk index
+  // t * chunks + q across stripes), processed in steps of teams x chunk_loop chunks; a step's chunks
+  // are split evenly over the teams, so the last (short) step costs ~1 chunk, not a whole tile.
+  s << "  const u32 teams = " << teams << "u, per = " << teams << "u * " << M << "u;\n";
+  s << "  const u32 total = stripes * chunks;\n";
+  s << "  const u32 per_cta = (total + gridDim.x - 1u) / gridDim.x;\n";
+  s << "  const u32 c0 = blockIdx.x * per_cta, c1 = min(total, c0 + per_cta);\n";
   s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (2u * PM_QMAX * 1024u);\n";
-  s << "  const u32 lbuf = sbuf + lane * 16u;\n";
   s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en();\n";
   s << "  u32 pb = 0u;\n";
-  // first prefetch: first stage of the first tile
   int first_sid = -1;
   for (size_t g = 0; g < groups.size() && first_sid < 0; g++)
     if (!gstages[g].empty()) first_sid = gstages[g][0];
   if (first_sid >= 0) {
-    s << "  if (blockIdx.x < tiles) {\n";
-    s << "    const u64 t0 = blockIdx.x / tps;\n";
-    s << "    const u32 q0 = (blockIdx.x - (u32)t0 * tps) * per + team * " << M << "u;\n";
-    emit_issue(s, first_sid, "t0", "q0", "0u", "    ");
+    s << "  if (c0 < c1) {\n";
+    s << "    const u32 n0 = min(per, c1 - c0), mt0 = (n0 + teams - 1u) / teams;\n";
+    emit_issue(s, first_sid, "c0 + team * mt0", "team * mt0 < n0", "0u", "    ");
     s << "  }\n";
   }
   s << "  pm_cp_commit();\n";
-  s << "  for (u32 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {\n";
-  s << "    const u64 t = tile / tps;\n";
-  s << "    const u32 qb = (tile - (u32)t * tps) * per + team * " << M << "u;\n";
-  s << "    const u32 ntile = tile + gridDim.x;\n";
-  s << "    const u64 tn = ntile / tps;\n";
-  s << "    const u32 qn = (ntile - (u32)tn * tps) * per + team * " << M << "u;\n";
+  s << "  for (u32 base = c0; base < c1; base += per) {\n";
+  s << "    const u32 n = min(per, c1 - base), mt = (n + teams - 1u) / teams;\n";
+  s << "    const u32 tb = base + team * mt;\n";
+  s << "    const u32 cnt = team * mt < n ? min(mt, n - team * mt) : 0u;\n";
+  s << "    const u32 nbase = base + per;\n";
+  s << "    const u32 nn = nbase < c1 ? min(per, c1 - nbase) : 0u, nmt = (nn + teams - 1u) / teams;\n";
   for (size_t g = 0; g < groups.size(); g++) {
     const Group &G = groups[g];
     const int mall = (int)G.rows.size();
@@ -406,10 +409,12 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
       if (!gstages[g2].empty()) { next_g = (int)g2; break; }
     if (o.sync_groups) s << "    __syncthreads();\n";
     s << "    #pragma unroll 1\n";
-    s << "    for (u32 m = 0; m < " << M << "u; m++) {\n";
-    s << "      const u32 q = qb + m;\n";
+    s << "    for (u32 m = 0; m < cnt; m++) {\n";
+    s << "      const u32 gi = tb + m;\n";
+    s << "      const u64 t = gi / chunks;\n";
+    s << "      const u32 q = gi - (u32)t * chunks;\n";
     s << "      const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
-    s << "      const bool v0 = q < chunks && o0 < S, v1 = q < chunks && o1 < S;\n";
+    s << "      const bool v0 = o0 < S, v1 = o1 < S;\n";
     s << "      switch (rank) {\n";
     for (int rk = 0; rk < T; rk++) {
       const int r0 = mall * rk / T, r1 = mall * (rk + 1) / T;
@@ -438,16 +443,16 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
         s << "          " << (T > 1 ? "pm_team_sync(1u + team, PM_T * 32u);" : "__syncwarp();") << "\n";
         // prefetch the successor stage into the other buffer
         if (sj + 1 < gstages[g].size()) {
-          emit_issue(s, gstages[g][sj + 1], "t", "q", "pb ^ 1u", "          ");
+          emit_issue(s, gstages[g][sj + 1], "gi", "true", "pb ^ 1u", "          ");
         } else {
-          s << "          if (m + 1u < " << M << "u) {\n";
-          emit_issue(s, gstages[g][0], "t", "q + 1u", "pb ^ 1u", "            ");
+          s << "          if (m + 1u < cnt) {\n";
+          emit_issue(s, gstages[g][0], "gi + 1u", "true", "pb ^ 1u", "            ");
           s << "          } else {\n";
           if (next_g >= 0) {
-            emit_issue(s, gstages[next_g][0], "t", "qb", "pb ^ 1u", "            ");
+            emit_issue(s, gstages[next_g][0], "tb", "true", "pb ^ 1u", "            ");
           } else if (first_sid >= 0) {
-            s << "            if (ntile < tiles) {\n";
-            emit_issue(s, first_sid, "tn", "qn", "pb ^ 1u", "              ");
+            s << "            if (team * nmt < nn) {\n";
+            emit_issue(s, first_sid, "nbase + team * nmt", "true", "pb ^ 1u", "              ");
             s << "            }\n";
           }
           s << "          }\n";

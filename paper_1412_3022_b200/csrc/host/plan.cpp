@@ -206,11 +206,9 @@ int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides
     }
     uint64_t S64 = S;
     void *args[] = {buf.data(), &S64, (void *)&ns, (void *)&chunks};
-    const uint64_t warps_per_block = k.tpb / 32;
-    const uint64_t per_tile = warps_per_block * std::max(1, k.chunk_loop);
-    const uint64_t tiles = (uint64_t)ns * ((chunks + per_tile - 1) / per_tile);
+    // the kernel splits the ns * chunks chunk range evenly over the CTAs
     uint64_t grid = (uint64_t)k.sms * k.blocks_per_sm;
-    grid = std::min<uint64_t>(grid, tiles);
+    grid = std::min<uint64_t>(grid, (uint64_t)ns * chunks);
     grid = std::max<uint64_t>(grid, 1);
     CUresult cr = drv().LaunchKernel((CUfunction)k.function, (unsigned)grid, 1, 1, k.tpb, 1, 1, (unsigned)k.smem, (CUstream)stream, args,
                                  nullptr);

@@ -38,12 +38,12 @@ struct PlanSpec {
 struct GenOptions {
   int max_rows = 8;      // output blocks per group (8 planes each in registers)
   int in_block = 14;     // loaded blocks per stage (shared-memory buffer of in_block KiB, x2)
-  int warps = 8;         // warps per CTA (capped by the 220 KiB shared-memory budget)
+  int warps = 12;        // warps per CTA (capped by the 220 KiB shared-memory budget)
   int tpb = 256;         // (derived) threads per CTA
   bool cse = true;       // Paar CSE (false: naive per-row XOR chains)
   bool sync_groups = true;  // __syncthreads() before each group: warps of a CTA execute the same code
   int sync_every = 0;       // also sync every N emitted XOR statements (0 = off)
-  int chunk_loop = 8;       // chunks per team per group (loop: instruction reuse)
+  int chunk_loop = 24;      // chunks per team per group (loop: instruction reuse)
   int team = 2;             // warps sharing one chunk's stage buffer (each computes 1/team of the rows)
   int ld_hint = 1;          // 0: __ldg/__stcs; 1: L2 evict-first cache-hinted loads/stores
 };

@@ -71,9 +71,15 @@ def _precompile_one(args):
     return args, rc
 
 
-def precompile(configs=PRECOMPILE):
-    """NVRTC-compile the encode kernels of `configs` into paper_1412_3022_b200/kcache (no GPU)."""
+def precompile(configs=PRECOMPILE, clean=True):
+    """NVRTC-compile the encode kernels of `configs` into paper_1412_3022_b200/kcache (no GPU).
+    clean=True first drops cubins of earlier generator versions (the cache is keyed by source)."""
     from multiprocessing import get_context
+    kdir = os.path.join(HERE, "kcache")
+    if clean and os.path.isdir(kdir):
+        for f in os.listdir(kdir):
+            if f.endswith(".cubin"):
+                os.remove(os.path.join(kdir, f))
     with get_context("spawn").Pool(min(len(configs), os.cpu_count() or 4)) as pool:
         res = pool.map(_precompile_one, configs)
     bad = [r for r in res if r[1] != 0]

@@ -119,7 +119,7 @@ void emit_slp_lazy(std::ostringstream &s, const Slp &p, const std::vector<std::s
   const int nin = p.n_in, nt = (int)p.tmp.size(), nr = (int)p.rows.size();
   const int nst = nt + nr;
   std::vector<std::vector<int>> ops(nst);
-  for (int i = 0; i < nt; i++) ops[i] = {p.tmp[i][0], p.tmp[i][1]};
+  for (int i = 0; i < nt; i++) ops[i] = p.tmp[i];
   for (int r = 0; r < nr; r++) ops[nt + r] = p.rows[r];
   std::vector<int> uses(nin + nt, 0);
   for (auto &o : ops)
@@ -158,8 +158,11 @@ void emit_slp_lazy(std::ostringstream &s, const Slp &p, const std::vector<std::s
       if (x < nin) base_live[x] = uses[x] > 0;
     }
     if (st < nt) {
-      std::string a = nm(ops[st][0]), b = nm(ops[st][1]);
-      s << "    const u32 " << tpref << st << " = " << a << " ^ " << b << ";\n";
+      std::vector<std::string> on;
+      for (int x : ops[st]) on.push_back(nm(x));
+      s << "    const u32 " << tpref << st << " = ";
+      for (size_t j = 0; j < on.size(); j++) s << (j ? " ^ " : "") << on[j];
+      s << ";\n";
       have[nin + st] = 1;
     } else {
       const int r = st - nt;
@@ -191,7 +194,7 @@ void emit_slp(std::ostringstream &s, const Slp &p, const std::vector<std::string
 }
 
 Slp make_slp(int n_in, const std::vector<std::vector<int>> &rows, bool cse) {
-  if (cse) return paar(n_in, rows);
+  if (cse) return cse3(n_in, rows);
   Slp s;
   s.n_in = n_in;
   s.rows = rows;

@@ -16,13 +16,19 @@ namespace pmrc {
 
 struct Slp {
   int n_in = 0;                          // base signals 0..n_in-1
-  std::vector<std::array<int, 2>> tmp;   // signal n_in+i = tmp[i][0] ^ tmp[i][1]
+  std::vector<std::vector<int>> tmp;     // signal n_in+i = XOR of tmp[i] (2 or 3 signals)
   std::vector<std::vector<int>> rows;    // each output = XOR of these signals (empty = 0)
   long xor2() const;                     // 2-input XOR count
+  long lop3() const;                     // 3-input LOP3 count (ternary trees)
 };
 
 // rows_in[r] = sorted list of base signals XORed into output r
 Slp paar(int n_in, const std::vector<std::vector<int>> &rows_in);
+
+// LOP3-aware CSE: greedily materialise the signal pair (used by >= 3 rows, saves ~r/2 - 1 LOP3) or
+// triple (used by >= 2 rows, saves r - 1) with the best saving; triples are found by extending the
+// top pairs with the best third signal among the rows that contain them.
+Slp cse3(int n_in, const std::vector<std::vector<int>> &rows_in);
 
 // naive 3-input-LOP3 count of a bit matrix row set: sum ceil((ones-1)/2)
 long naive_lop3(const std::vector<std::vector<int>> &rows);

@@ -203,6 +203,7 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "ld_hint") c->gen.ld_hint = v;
         if (key == "chunk_loop" && v > 0) c->gen.chunk_loop = v;
         if (key == "team" && v > 0) c->gen.team = v;
+        if (key == "fold") c->gen.fold = v != 0;
       }
       pos = e + 1;
     }

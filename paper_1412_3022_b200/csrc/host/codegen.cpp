@@ -124,8 +124,14 @@ void emit_slp_lazy(std::ostringstream &s, const Slp &p, const std::vector<std::s
   std::vector<int> uses(nin + nt, 0);
   for (auto &o : ops)
     for (int x : o) uses[x]++;
-  std::vector<char> done(nst, 0), have(nin + nt, 0), base_live(nin, 0);
+  std::vector<char> done(nst, 0), have(nin + nt, 0);
   for (int i = 0; i < nin; i++) have[i] = 1;
+  // base signals come in quads (one LDS.128 = 4 registers, live until all 4 planes are done)
+  std::vector<int> quad_uses((nin + 3) / 4, 0);
+  std::vector<char> quad_live((nin + 3) / 4, 0);
+  for (auto &o : ops)
+    for (int x : o)
+      if (x < nin) quad_uses[x / 4]++;
   auto nm = [&](int sig) -> std::string {
     if (sig < nin) {
       need(base[sig]);
@@ -138,6 +144,7 @@ void emit_slp_lazy(std::ostringstream &s, const Slp &p, const std::vector<std::s
       if (!have[x]) return false;
     return true;
   };
+  std::vector<int> qcount((nin + 3) / 4, 0);
   for (int step = 0; step < nst; step++) {
     int best = -1, bestscore = 1 << 30;
     for (int st = 0; st < nst; st++) {
@@ -146,8 +153,16 @@ void emit_slp_lazy(std::ostringstream &s, const Slp &p, const std::vector<std::s
       if (st < nt) sc += 1;                                   // defines a temp
       else if (!accumulate && !ops[st].empty()) sc += 1;      // defines an output (stays live)
       for (int x : ops[st]) {
-        if (uses[x] == 1) sc -= 1;                            // last use: dies here
-        if (x < nin && !base_live[x]) sc += 1;                // brings a plane in
+        if (x >= nin && uses[x] == 1) sc -= 1;                // a temp's last use
+        if (x < nin) qcount[x / 4]++;
+      }
+      for (int x : ops[st]) {
+        if (x >= nin) continue;
+        const int q = x / 4;
+        if (!qcount[q]) continue;
+        if (!quad_live[q]) sc += 4;                           // loads a quad
+        if (quad_uses[q] == qcount[q]) sc -= 4;               // the quad's last use
+        qcount[q] = 0;
       }
       if (sc < bestscore || (sc == bestscore && st < best)) { bestscore = sc; best = st; }
     }
@@ -155,7 +170,10 @@ void emit_slp_lazy(std::ostringstream &s, const Slp &p, const std::vector<std::s
     done[st] = 1;
     for (int x : ops[st]) {
       uses[x]--;
-      if (x < nin) base_live[x] = uses[x] > 0;
+      if (x < nin) {
+        quad_uses[x / 4]--;
+        quad_live[x / 4] = quad_uses[x / 4] > 0;
+      }
     }
     if (st < nt) {
       std::vector<std::string> on;
@@ -188,6 +206,70 @@ void emit_slp_lazy(std::ostringstream &s, const Slp &p, const std::vector<std::s
     }
   }
 }
+// Eager-fold emission: temps in creation order; every operand that becomes available (a temp when
+// created, a plane quad when loaded) is folded into the rows that use it as soon as a row has two
+// pending operands (o ^= a ^ b: one 3-input LOP3), so temps and plane quads die right after their
+// last consumer instead of living until a row's single big expression.
+template <class Need>
+void emit_slp_fold(std::ostringstream &s, const Slp &p, const std::vector<std::string> &base,
+                   const std::vector<std::string> &outs, bool accumulate, const std::string &tpref, Need need) {
+  const int nin = p.n_in, nt = (int)p.tmp.size(), nr = (int)p.rows.size();
+  std::vector<std::vector<int>> rows_of(nin + nt);
+  for (int r = 0; r < nr; r++)
+    for (int x : p.rows[r]) rows_of[x].push_back(r);
+  std::vector<std::vector<int>> pending(nr);
+  std::vector<char> started(nr, accumulate ? 1 : 0), quad_done((nin + 3) / 4, 0);
+  auto name = [&](int sig) { return sig < nin ? base[sig] : tpref + std::to_string(sig - nin); };
+  auto try_fold = [&](int r) {
+    auto &pd = pending[r];
+    if (!started[r]) {
+      if (pd.size() < 3) return;
+      s << "    " << outs[r] << " = " << name(pd[0]) << " ^ " << name(pd[1]) << " ^ " << name(pd[2]) << ";\n";
+      pd.erase(pd.begin(), pd.begin() + 3);
+      started[r] = 1;
+    }
+    while (pd.size() >= 2) {
+      s << "    " << outs[r] << " ^= " << name(pd[0]) << " ^ " << name(pd[1]) << ";\n";
+      pd.erase(pd.begin(), pd.begin() + 2);
+    }
+  };
+  auto make_available = [&](int sig) {
+    for (int r : rows_of[sig]) {
+      pending[r].push_back(sig);
+      try_fold(r);
+    }
+  };
+  auto load_quad = [&](int q) {
+    if (quad_done[q]) return;
+    quad_done[q] = 1;
+    need(base[4 * q]);
+    for (int x = 4 * q; x < std::min(nin, 4 * q + 4); x++) make_available(x);
+  };
+  for (int i = 0; i < nt; i++) {
+    for (int x : p.tmp[i])
+      if (x < nin) load_quad(x / 4);
+    s << "    const u32 " << tpref << i << " = ";
+    for (size_t j = 0; j < p.tmp[i].size(); j++) s << (j ? " ^ " : "") << name(p.tmp[i][j]);
+    s << ";\n";
+    make_available(nin + i);
+  }
+  for (int r = 0; r < nr; r++)
+    for (int x : p.rows[r])
+      if (x < nin) load_quad(x / 4);
+  for (int r = 0; r < nr; r++) {
+    auto &pd = pending[r];
+    if (!started[r]) {
+      s << "    " << outs[r] << " = ";
+      if (pd.empty()) s << "0u";
+      for (size_t j = 0; j < pd.size(); j++) s << (j ? " ^ " : "") << name(pd[j]);
+      s << ";\n";
+    } else if (!pd.empty()) {
+      s << "    " << outs[r] << " ^= " << name(pd[0]) << ";\n";
+    }
+    pd.clear();
+  }
+}
+
 void emit_slp(std::ostringstream &s, const Slp &p, const std::vector<std::string> &base,
               const std::vector<std::string> &outs, bool accumulate, const std::string &tpref) {
   emit_slp_lazy(s, p, base, outs, accumulate, tpref, [](const std::string &) {});
@@ -527,7 +609,10 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
           for (int h = 0; h < 2 * nblk; h++)
             if (used_half[h] && !loaded[h]) need("P" + std::to_string(h) + ".x");
           net << body.str();
-          emit_slp_lazy(net, sl, base, outs, !first, "t", need);
+          if (o.fold)
+            emit_slp_fold(net, sl, base, outs, !first, "t", need);
+          else
+            emit_slp_lazy(net, sl, base, outs, !first, "t", need);
           s << net.str();
           first = false;
         }

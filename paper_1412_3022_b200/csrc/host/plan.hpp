@@ -45,7 +45,8 @@ struct GenOptions {
   int sync_every = 0;       // also sync every N emitted XOR statements (0 = off)
   int chunk_loop = 24;      // chunks per team per group (loop: instruction reuse)
   int team = 2;             // warps sharing one chunk's stage buffer (each computes 1/team of the rows)
-  int ld_hint = 1;          // 0: __ldg/__stcs; 1: L2 evict-first cache-hinted loads/stores
+  int ld_hint = 1;
+  bool fold = true;         // eager-fold emission of XOR networks (low register pressure)          // 0: __ldg/__stcs; 1: L2 evict-first cache-hinted loads/stores
 };
 
 struct GenStats {

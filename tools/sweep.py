@@ -1,0 +1,186 @@
+#!/usr/bin/env python3
+"""Throughput of the other BASELINE.json configurations through the C ABI (kernel-only, CUDA
+events, inputs resident, >= 1 GiB per measurement so L2 does not hold the data):
+
+  config 3: MBR k=8 d=14 n=16, 1 GiB, 256 KiB sub-blocks: encode, then decode from a random 8-subset
+  config 4: MSR k=8 d=14 n=16, 1 GiB, 1 MiB sub-blocks: repair of a random lost node from a random
+            non-singular 14-helper set (R10), and decode from a random 8-subset
+  config 5: encode sweep: (MSR sparse, MBR) x k in {4, 8, 16} (d = 2k-2, n = 2k) x S, + RS(16,8)
+
+Normalisation (P:216 footnote, R14): encode/decode GB/s of k*alpha source blocks; repair GB/s of
+the alpha repaired blocks.  Each decode/repair result is checked bit-exactly against the encoded
+data on the device (torch.equal) before it is timed.  Prints one JSON line per measurement.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch
+
+import inputs
+import paper_1412_3022_b200 as pm
+
+MSR, VAN, MBR, RS = 0, 1, 2, 3
+
+
+def timed(fn, steps=10, warmup=3):
+    st = torch.cuda.current_stream()
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+class Job:
+    def __init__(self, kind, k, n, S, real=1 << 30, seed=5):
+        self.kind, self.k, self.n, self.S = kind, k, n, S
+        self.d = k if kind == RS else 2 * k - 2
+        t0 = time.time()
+        self.code = pm.pmrc_create(kind, k, self.d, n)
+        self.init_s = time.time() - t0
+        info = pm.pmrc_info(self.code)
+        self.alpha, self.B, self.P = info["alpha"], info["B"], info["parity_rows"]
+        self.stripes = -(-real // (self.B * S))
+        self.data = torch.empty((self.stripes, self.B, S), dtype=torch.uint8, device="cuda")
+        self.par = torch.empty((self.stripes, self.P, S), dtype=torch.uint8, device="cuda")
+        self.st = torch.cuda.current_stream().cuda_stream
+        inputs.fill_device(self.data.data_ptr(), self.data.numel(), seed, stream=self.st)
+        self.L = pm.pmrc_layout(self.code)
+        self._mbr = {}
+
+    def encode(self):
+        pm.pmrc_encode(self.code, self.data.data_ptr(), self.par.data_ptr(), self.S, self.stripes, self.st)
+
+    def piece(self, i):
+        a, S = self.alpha, self.S
+        if i >= self.k:
+            return (self.par.data_ptr() + (i - self.k) * a * S, self.P * S)
+        if self.kind != MBR:
+            return (self.data.data_ptr() + i * a * S, self.B * S)
+        if i not in self._mbr:   # MBR systematic node = row i of M(X) (R6), materialised once
+            idx = torch.tensor([int(v) - 1 for v in self.L[i]], device="cuda")
+            self._mbr[i] = self.data.index_select(1, idx).contiguous()
+        return (self._mbr[i].data_ptr(), a * S)
+
+    def piece_tensor(self, i):
+        a = self.alpha
+        if i >= self.k:
+            return self.par[:, (i - self.k) * a:(i - self.k + 1) * a]
+        if self.kind != MBR:
+            return self.data[:, i * a:(i + 1) * a]
+        self.piece(i)
+        return self._mbr[i]
+
+    def close(self):
+        pm.pmrc_destroy(self.code)
+
+
+def emit(d):
+    print(json.dumps(d), flush=True)
+
+
+def run_encode(kind, k, n, S, steps):
+    j = Job(kind, k, n, S)
+    ms = timed(j.encode, steps)
+    src = j.stripes * j.B * j.S
+    emit({"op": "encode", "kind": ["msr_sparse", "msr_vanilla", "mbr", "rs"][kind], "k": k, "n": n, "S": S,
+          "stripes": j.stripes, "ms": round(ms, 4), "GBps": round(src / ms / 1e6, 1), "init_s": round(j.init_s, 2)})
+    return j
+
+
+def run_decode(j, rng, steps, label):
+    ids = sorted(rng.choice(j.n, j.k, replace=False).tolist())
+    out = torch.zeros_like(j.data)
+    t0 = time.time()
+    nw = pm.pmrc_decode(j.code, ids, [j.piece(i) for i in ids], out.data_ptr(), j.S, j.stripes, j.st)
+    torch.cuda.synchronize()
+    init = time.time() - t0
+    lost = [i for i in range(j.k) if i not in ids]
+    if j.kind != MBR:
+        miss = [i * j.alpha + a for i in lost for a in range(j.alpha)]
+    else:
+        held = set()
+        for i in ids:
+            if i < j.k:
+                held |= {int(v) - 1 for v in j.L[i]}
+        miss = sorted(set(range(j.B)) - held)
+    ok = bool(torch.equal(out[:, miss], j.data[:, miss])) if miss else True
+    ms = timed(lambda: pm.pmrc_decode(j.code, ids, [j.piece(i) for i in ids], out.data_ptr(), j.S, j.stripes,
+                                      j.st), steps)
+    src = j.stripes * j.B * j.S   # decode throughput per k*alpha blocks of data
+    emit({"op": "decode", "config": label, "kind": ["msr_sparse", "msr_vanilla", "mbr", "rs"][j.kind], "k": j.k,
+          "n": j.n, "S": j.S, "survivors": ids, "blocks_written": nw, "bit_exact": ok, "ms": round(ms, 4),
+          "GBps": round(src / ms / 1e6, 1), "plan_init_s": round(init, 2)})
+
+
+def run_repair(j, rng, steps, label):
+    need = j.k if j.kind == RS else j.d
+    rejected = 0
+    while True:
+        f = int(rng.integers(j.n))
+        H = sorted(rng.choice([i for i in range(j.n) if i != f], need, replace=False).tolist())
+        out = torch.empty((j.stripes, j.alpha, j.S), dtype=torch.uint8, device="cuda")
+        t0 = time.time()
+        try:
+            pm.pmrc_repair(j.code, f, H, [j.piece(i) for i in H], (out.data_ptr(), j.alpha * j.S), j.S, j.stripes, j.st)
+        except pm.PmrcError as e:
+            if e.rc == pm.PMRC_ESINGULAR:
+                rejected += 1
+                continue
+            raise
+        torch.cuda.synchronize()
+        init = time.time() - t0
+        break
+    ok = bool(torch.equal(out, j.piece_tensor(f)))
+    ms = timed(lambda: pm.pmrc_repair(j.code, f, H, [j.piece(i) for i in H], (out.data_ptr(), j.alpha * j.S), j.S,
+                                      j.stripes, j.st), steps)
+    rep = j.stripes * j.alpha * j.S          # repair throughput per alpha repaired blocks
+    read = pm.pmrc_read_cost(j.code, f) * len(H) * j.stripes * j.S
+    emit({"op": "repair", "config": label, "kind": ["msr_sparse", "msr_vanilla", "mbr", "rs"][j.kind], "k": j.k,
+          "n": j.n, "S": j.S, "lost": f, "helpers": H, "singular_rejected": rejected, "bit_exact": ok,
+          "ms": round(ms, 4), "GBps_repaired": round(rep / ms / 1e6, 1), "GBps_read": round(read / ms / 1e6, 1),
+          "blocks_read_per_helper": pm.pmrc_read_cost(j.code, f), "plan_init_s": round(init, 2)})
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="3,4,5")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--sizes", default="4,16,64,256,1024,4096", help="config-5 sub-block sizes (KiB)")
+    ap.add_argument("--ks", default="4,8,16")
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    rng = inputs.rng(2026)
+    cfgs = set(args.configs.split(","))
+    if "3" in cfgs:
+        j = run_encode(MBR, 8, 16, 256 << 10, args.steps)
+        run_decode(j, rng, args.steps, "config3")
+        j.close()
+    if "4" in cfgs:
+        j = run_encode(MSR, 8, 16, 1 << 20, args.steps)
+        for _ in range(3):
+            run_repair(j, rng, args.steps, "config4")
+        run_decode(j, rng, args.steps, "config4")
+        j.close()
+    if "5" in cfgs:
+        for kind in (MSR, MBR):
+            for k in [int(x) for x in args.ks.split(",")]:
+                for kib in [int(x) for x in args.sizes.split(",")]:
+                    run_encode(kind, k, 2 * k, kib << 10, args.steps).close()
+        for kib in [int(x) for x in args.sizes.split(",")]:
+            run_encode(RS, 8, 16, kib << 10, args.steps).close()
+
+
+if __name__ == "__main__":
+    main()

@@ -148,6 +148,13 @@ int pmrc_precompile(const pmrc_code *c);
  * up to cap bytes (NUL-terminated if room) and the full length to *len. */
 int pmrc_encode_source(const pmrc_code *c, char *buf, size_t cap, size_t *len);
 
+/* Diagnostics of the encode kernel's CTA pacing (group-specialised layout): copies the device
+ * counter area (5 x E u64: progress counters, then per-(CTA, team) start / end globaltimer ns, ns
+ * spent pacing and pacing timeouts, the last four only with PMRC_GEN=trace=1) to host[0..cap) and
+ * its length to *n (0 if the encode kernel has no counters).  Synchronous (cudaMemcpy); not part
+ * of the data path. */
+int pmrc_debug_counters(const pmrc_code *c, unsigned long long *host, size_t cap, size_t *n);
+
 /* Number of kernels this library launched since load (for the bench's gpu_launches claim). */
 unsigned long long pmrc_launch_count(void);
 

@@ -21,7 +21,7 @@ MATRIX_PSI, MATRIX_G, MATRIX_GSYS, MATRIX_GPP, MATRIX_LAMBDA = 0, 1, 2, 3, 4
 EXPORTS = ["pmrc_create", "pmrc_destroy", "pmrc_info", "pmrc_matrix", "pmrc_layout", "pmrc_encode",
            "pmrc_encode_host", "pmrc_decode", "pmrc_repair", "pmrc_repair_project", "pmrc_repair_combine",
            "pmrc_read_cost", "pmrc_launch_count", "pmrc_strerror", "pmrc_last_error", "pmrc_precompile",
-           "pmrc_encode_source"]
+           "pmrc_encode_source", "pmrc_debug_counters"]
 
 
 class PmrcError(RuntimeError):
@@ -76,6 +76,7 @@ def lib():
             "pmrc_launch_count": ([], ctypes.c_ulonglong),
             "pmrc_precompile": ([P], I),
             "pmrc_encode_source": ([P, P, Z, ctypes.POINTER(ctypes.c_size_t)], I),
+            "pmrc_debug_counters": ([P, P, Z, ctypes.POINTER(ctypes.c_size_t)], I),
             "pmrc_strerror": ([I], ctypes.c_char_p),
             "pmrc_last_error": ([], ctypes.c_char_p),
         }
@@ -190,6 +191,15 @@ def pmrc_encode_source(code):
     buf = ctypes.create_string_buffer(n.value + 1)
     _check(lib().pmrc_encode_source(code, buf, n.value + 1, ctypes.byref(n)), "pmrc_encode_source")
     return buf.value.decode()
+
+
+def pmrc_debug_counters(code):
+    """Pacing counters / trace of the encode kernel as a list of ints (diagnostics)."""
+    n = ctypes.c_size_t(0)
+    _check(lib().pmrc_debug_counters(code, None, 0, ctypes.byref(n)), "pmrc_debug_counters")
+    buf = (ctypes.c_ulonglong * max(1, n.value))()
+    _check(lib().pmrc_debug_counters(code, buf, n.value, ctypes.byref(n)), "pmrc_debug_counters")
+    return list(buf[: n.value])
 
 
 def pmrc_launch_count():

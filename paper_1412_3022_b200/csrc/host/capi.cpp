@@ -204,6 +204,9 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "chunk_loop" && v > 0) c->gen.chunk_loop = v;
         if (key == "team" && v > 0) c->gen.team = v;
         if (key == "fold") c->gen.fold = v != 0;
+        if (key == "layout") c->gen.layout = v;
+        if (key == "pace_lag") c->gen.pace_lag = v;
+        if (key == "trace") c->gen.trace = v != 0;
       }
       pos = e + 1;
     }
@@ -268,6 +271,20 @@ int pmrc_precompile(const pmrc_code *c) {
   std::string err;
   int rc = precompile_kernel(c->enc_spec, c->gen, err);
   if (rc) return fail(rc, err);
+  return PMRC_OK;
+}
+
+int pmrc_debug_counters(const pmrc_code *c, unsigned long long *host, size_t cap, size_t *n) {
+  if (!c || !n) return fail(PMRC_EINVAL, "NULL argument");
+  *n = 0;
+  if (!c->enc_built || !c->enc.pace) return PMRC_OK;
+  const size_t total = c->enc.pace_entries * 6;
+  *n = total;
+  if (!host || cap < total) return PMRC_OK;
+  if (cudaMemcpy(host, c->enc.pace, total * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(PMRC_ECUDA, "cudaMemcpy(pace counters)");
+  }
   return PMRC_OK;
 }
 

@@ -18,6 +18,7 @@
 //     LOP3 mux + IMAD shifts) into 8 bit planes; the XOR network reads planes with LDS.128, keeps
 //     the group's 8 x 8 output planes in registers, then transposes back and stores 16-B vectors.
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <sstream>
 
@@ -95,6 +96,30 @@ static __device__ __forceinline__ void pm_bar_wait(u32 bar, u32 parity) {
     asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                  : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
   } while (!ok);
+}
+// pacing of group-specialised CTAs (layout 1): wait until the n peer counters p[i * stride] reach
+// `want`; bounded (a peer that is not resident must never deadlock us): after a timeout the caller
+// stops pacing for the rest of the launch.  Counters are (epoch << 32 | chunks done).
+static __device__ __forceinline__ bool pm_pace(const u64 *p, u32 stride, u32 n, u64 want, u32 lane) {
+  for (u32 spin = 0; spin < 2048u; spin++) {
+    bool ok = true;
+    for (u32 i = lane; i < n; i += 32u) {
+      u64 v;
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p + (u64)i * stride) : "memory");
+      ok = ok && v >= want;
+    }
+    if (__all_sync(0xffffffffu, ok)) return true;
+    __nanosleep(128);
+  }
+  return false;
+}
+static __device__ __forceinline__ u64 pm_gtime() {
+  u64 t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+static __device__ __forceinline__ void pm_pace_post(u64 *p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
 static __device__ __forceinline__ void pm_bulk(u32 dst, const void *src, u32 bytes, u32 bar, bool ef, u64 pol) {
   if (ef)
@@ -456,50 +481,17 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
   const int TPB = 32 * std::max(T, o.warps);
   const int teams = TPB / 32 / T;
   s << "extern \"C\" __global__ void __launch_bounds__(" << TPB << ", 1) pmrc_kernel(const __grid_constant__ Slots R, "
-       "const u64 S, const u32 stripes, const u32 chunks) {\n";
+       "const u64 S, const u32 stripes, const u32 chunks, u64 *__restrict__ pace, const u32 epoch) {\n";
   s << "  extern __shared__ __align__(1024) unsigned char pm_smem[];\n";
   s << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, team = warp / PM_T, rank = warp - team * PM_T;\n";
-  // Work distribution: CTA b owns the contiguous global chunk range [c0, c1) (chunk index
-  // t * chunks + q across stripes), processed in steps of teams x chunk_loop chunks; a step's chunks
-  // are split evenly over the teams, so the last (short) step costs ~1 chunk, not a whole tile.
-  s << "  const u32 teams = " << teams << "u, per = " << teams << "u * " << M << "u;\n";
-  s << "  const u32 total = stripes * chunks;\n";
-  s << "  const u32 per_cta = (total + gridDim.x - 1u) / gridDim.x;\n";
-  s << "  const u32 c0 = blockIdx.x * per_cta, c1 = min(total, c0 + per_cta);\n";
-  s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (2u * PM_QMAX * 1024u);\n";
-  s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en();\n";
-  s << "  u32 pb = 0u;\n";
   int first_sid = -1;
   for (size_t g = 0; g < groups.size() && first_sid < 0; g++)
     if (!gstages[g].empty()) first_sid = gstages[g][0];
-  if (first_sid >= 0) {
-    s << "  if (c0 < c1) {\n";
-    s << "    const u32 n0 = min(per, c1 - c0), mt0 = (n0 + teams - 1u) / teams;\n";
-    emit_issue(s, first_sid, "c0 + team * mt0", "team * mt0 < n0", "0u", "    ");
-    s << "  }\n";
-  }
-  s << "  pm_cp_commit();\n";
-  s << "  for (u32 base = c0; base < c1; base += per) {\n";
-  s << "    const u32 n = min(per, c1 - base), mt = (n + teams - 1u) / teams;\n";
-  s << "    const u32 tb = base + team * mt;\n";
-  s << "    const u32 cnt = team * mt < n ? min(mt, n - team * mt) : 0u;\n";
-  s << "    const u32 nbase = base + per;\n";
-  s << "    const u32 nn = nbase < c1 ? min(per, c1 - nbase) : 0u, nmt = (nn + teams - 1u) / teams;\n";
-  for (size_t g = 0; g < groups.size(); g++) {
+  // the work of one (group, chunk) item: per stage wait -> transpose -> team sync -> prefetch(g, sj)
+  // -> XOR network; then transpose back and store.  Needs gi, t, q, o0, o1, v0, v1 in scope.
+  auto emit_body = [&](size_t g, const std::function<void(size_t, size_t)> &prefetch) {
     const Group &G = groups[g];
     const int mall = (int)G.rows.size();
-    // successor group with stages (for the prefetch after this group's last stage at m = M-1)
-    int next_g = -1;
-    for (size_t g2 = g + 1; g2 < groups.size(); g2++)
-      if (!gstages[g2].empty()) { next_g = (int)g2; break; }
-    if (o.sync_groups) s << "    __syncthreads();\n";
-    s << "    #pragma unroll 1\n";
-    s << "    for (u32 m = 0; m < cnt; m++) {\n";
-    s << "      const u32 gi = tb + m;\n";
-    s << "      const u64 t = gi / chunks;\n";
-    s << "      const u32 q = gi - (u32)t * chunks;\n";
-    s << "      const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
-    s << "      const bool v0 = o0 < S, v1 = o1 < S;\n";
     s << "      switch (rank) {\n";
     for (int rk = 0; rk < T; rk++) {
       const int r0 = mall * rk / T, r1 = mall * (rk + 1) / T;
@@ -527,21 +519,7 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
         s << "          pm_transpose_in(buf + lane * 16u, " << nblk * rk / T << "u, " << nblk * (rk + 1) / T << "u);\n";
         s << "          " << (T > 1 ? "pm_team_sync(1u + team, PM_T * 32u);" : "__syncwarp();") << "\n";
         // prefetch the successor stage into the other buffer
-        if (sj + 1 < gstages[g].size()) {
-          emit_issue(s, gstages[g][sj + 1], "gi", "true", "pb ^ 1u", "          ");
-        } else {
-          s << "          if (m + 1u < cnt) {\n";
-          emit_issue(s, gstages[g][0], "gi + 1u", "true", "pb ^ 1u", "            ");
-          s << "          } else {\n";
-          if (next_g >= 0) {
-            emit_issue(s, gstages[next_g][0], "tb", "true", "pb ^ 1u", "            ");
-          } else if (first_sid >= 0) {
-            s << "            if (team * nmt < nn) {\n";
-            emit_issue(s, first_sid, "nbase + team * nmt", "true", "pb ^ 1u", "              ");
-            s << "            }\n";
-          }
-          s << "          }\n";
-        }
+        prefetch(g, sj);
         s << "          pm_cp_commit();\n";
         s << "          const u32 pl = buf + lane * 16u;\n";
         if (m > 0) {
@@ -641,9 +619,148 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
       s << "      } break;\n";
     }
     s << "      default: break;\n      }\n";
+  };
+  if (o.layout == 0) {
+  // layout 0: CTA b owns the contiguous global chunk range [c0, c1) (chunk index t * chunks + q
+  // across stripes), processed in steps of teams x chunk_loop chunks, all groups in turn; a step's
+  // chunks are split evenly over the teams, so the last (short) step costs ~1 chunk, not a tile.
+  s << "  const u32 teams = " << teams << "u, per = " << teams << "u * " << M << "u;\n";
+  s << "  const u32 total = stripes * chunks;\n";
+  s << "  const u32 per_cta = (total + gridDim.x - 1u) / gridDim.x;\n";
+  s << "  const u32 c0 = blockIdx.x * per_cta, c1 = min(total, c0 + per_cta);\n";
+  s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (2u * PM_QMAX * 1024u);\n";
+  s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en();\n";
+  s << "  u32 pb = 0u;\n";
+  if (first_sid >= 0) {
+    s << "  if (c0 < c1) {\n";
+    s << "    const u32 n0 = min(per, c1 - c0), mt0 = (n0 + teams - 1u) / teams;\n";
+    emit_issue(s, first_sid, "c0 + team * mt0", "team * mt0 < n0", "0u", "    ");
+    s << "  }\n";
+  }
+  s << "  pm_cp_commit();\n";
+  s << "  for (u32 base = c0; base < c1; base += per) {\n";
+  s << "    const u32 n = min(per, c1 - base), mt = (n + teams - 1u) / teams;\n";
+  s << "    const u32 tb = base + team * mt;\n";
+  s << "    const u32 cnt = team * mt < n ? min(mt, n - team * mt) : 0u;\n";
+  s << "    const u32 nbase = base + per;\n";
+  s << "    const u32 nn = nbase < c1 ? min(per, c1 - nbase) : 0u, nmt = (nn + teams - 1u) / teams;\n";
+  for (size_t g = 0; g < groups.size(); g++) {
+    // successor group with stages (for the prefetch after this group's last stage at m = M-1)
+    int next_g = -1;
+    for (size_t g2 = g + 1; g2 < groups.size(); g2++)
+      if (!gstages[g2].empty()) { next_g = (int)g2; break; }
+    if (o.sync_groups) s << "    __syncthreads();\n";
+    s << "    #pragma unroll 1\n";
+    s << "    for (u32 m = 0; m < cnt; m++) {\n";
+    s << "      const u32 gi = tb + m;\n";
+    s << "      const u64 t = gi / chunks;\n";
+    s << "      const u32 q = gi - (u32)t * chunks;\n";
+    s << "      const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
+    s << "      const bool v0 = o0 < S, v1 = o1 < S;\n";
+    emit_body(g, [&](size_t gg, size_t sj) {
+      if (sj + 1 < gstages[gg].size()) {
+        emit_issue(s, gstages[gg][sj + 1], "gi", "true", "pb ^ 1u", "          ");
+        return;
+      }
+      s << "          if (m + 1u < cnt) {\n";
+      emit_issue(s, gstages[gg][0], "gi + 1u", "true", "pb ^ 1u", "            ");
+      s << "          } else {\n";
+      if (next_g >= 0) {
+        emit_issue(s, gstages[next_g][0], "tb", "true", "pb ^ 1u", "            ");
+      } else if (first_sid >= 0) {
+        s << "            if (team * nmt < nn) {\n";
+        emit_issue(s, first_sid, "nbase + team * nmt", "true", "pb ^ 1u", "              ");
+        s << "            }\n";
+      }
+      s << "          }\n";
+    });
     s << "    }\n";
   }
   s << "  }\n}\n";
+  } else {
+  // layout 1 (group-specialised CTAs): CTA b computes group g = b / spg only, over chunk range
+  // r = b % spg of the global chunk index; the spg ranges are the same for every group, so the
+  // CTAs of different groups that read a shared input block do so at about the same time (the
+  // second read hits L2) and each SM only ever executes one group's code (instruction cache).
+  // Teams interleave over the range (team, team + teams, ...) so all groups advance in step.
+  s << "  const u32 teams = " << teams << "u;\n";
+  s << "  const u32 spg = gridDim.x / " << groups.size() << "u, g = blockIdx.x / spg, r = blockIdx.x - g * spg;\n";
+  s << "  const u32 total = stripes * chunks;\n";
+  s << "  const u32 c0 = (u32)((u64)total * r / spg), c1 = (u32)((u64)total * (r + 1u) / spg);\n";
+  s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (2u * PM_QMAX * 1024u);\n";
+  s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en();\n";
+  s << "  u32 pb = 0u;\n";
+  s << "  bool pacing = pace != 0;\n";
+  if (o.trace) s << "  const u64 tr_t0 = pm_gtime(); u64 tr_wait = 0; u32 tr_fail = 0;\n";
+  s << "  switch (g) {\n";
+  for (size_t g = 0; g < groups.size(); g++) {
+    s << "  case " << g << ": {\n";
+    if (!gstages[g].empty()) {
+      s << "    if (c0 + team < c1) {\n";
+      emit_issue(s, gstages[g][0], "c0 + team", "true", "0u", "      ");
+      s << "    }\n";
+    }
+    s << "    pm_cp_commit();\n";
+    s << "    #pragma unroll 1\n";
+    s << "    for (u32 gi = c0 + team, kk = 0; gi < c1; gi += teams, kk++) {\n";
+    const bool pace_async = o.pace_lag > 0 && groups.size() <= 32;
+    if (o.pace_lag > 0) {
+      // stay within pace_lag chunks of the slowest CTA of the same range (all groups).  Only rank 0
+      // paces (rank 1 meets it at the team barrier).  The peers' counters for the next iteration
+      // are loaded here and tested after this iteration's work, so the L2 round trip (several us
+      // under full HBM load) overlaps the XOR network instead of stalling the team.
+      if (o.trace)
+        s << "      if (r == 0u && team == 0u && rank == 0u && lane == 0u && kk < 256u) pace[5u * 4096u + g * 256u + kk] = pm_gtime();\n";
+      if (pace_async) {
+        s << "      u64 pv = ~0ull;\n";
+        s << "      if (pacing && rank == 0u && lane < " << groups.size() << "u)\n";
+        s << "        asm volatile(\"ld.relaxed.gpu.global.u64 %0, [%1];\" : \"=l\"(pv) : \"l\"(pace + (r + lane * spg) * teams + team));\n";
+      } else {
+        s << "      if (pacing && rank == 0u && kk > " << o.pace_lag << "u) {\n";
+        if (o.trace) s << "        const u64 tw = pm_gtime();\n";
+        s << "        pacing = pm_pace(pace + r * teams + team, spg * teams, " << groups.size()
+          << "u, ((u64)epoch << 32) | (kk - " << o.pace_lag << "u), lane);\n";
+        if (o.trace) s << "        tr_wait += pm_gtime() - tw; tr_fail += pacing ? 0u : 1u;\n";
+        s << "      }\n";
+      }
+    }
+    s << "      const u64 t = gi / chunks;\n";
+    s << "      const u32 q = gi - (u32)t * chunks;\n";
+    s << "      const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
+    s << "      const bool v0 = o0 < S, v1 = o1 < S;\n";
+    emit_body(g, [&](size_t gg, size_t sj) {
+      if (sj + 1 < gstages[gg].size()) {
+        emit_issue(s, gstages[gg][sj + 1], "gi", "true", "pb ^ 1u", "          ");
+        return;
+      }
+      s << "          if (gi + teams < c1) {\n";
+      emit_issue(s, gstages[gg][0], "gi + teams", "true", "pb ^ 1u", "            ");
+      s << "          }\n";
+    });
+    if (o.pace_lag > 0)
+      s << "      if (pace && rank == 0u && lane == 0u) pm_pace_post(pace + blockIdx.x * teams + team, ((u64)epoch << 32) | (kk + 1u));\n";
+    if (pace_async) {
+      s << "      if (pacing && rank == 0u && kk + 1u > " << o.pace_lag << "u) {\n";
+      s << "        const u64 want = ((u64)epoch << 32) | (kk + 1u - " << o.pace_lag << "u);\n";
+      s << "        if (!__all_sync(0xffffffffu, pv >= want)) {\n";
+      if (o.trace) s << "          const u64 tw = pm_gtime();\n";
+      s << "          pacing = pm_pace(pace + r * teams + team, spg * teams, " << groups.size() << "u, want, lane);\n";
+      if (o.trace) s << "          tr_wait += pm_gtime() - tw; tr_fail += pacing ? 0u : 1u;\n";
+      s << "        }\n      }\n";
+    }
+    s << "    }\n";
+    s << "  } break;\n";
+  }
+  s << "  default: break;\n  }\n";
+  if (o.trace) {
+    // diagnostics (E = 4096 entries per field, plan.cpp): [E + i] start, [2E + i] end (globaltimer ns), [3E + i] ns spent pacing, [4E + i] timeouts
+    s << "  if (pace && rank == 0u && lane == 0u) {\n";
+    s << "    const u32 E = 4096u, i = blockIdx.x * teams + team;\n";
+    s << "    pace[E + i] = tr_t0; pace[2u * E + i] = pm_gtime(); pace[3u * E + i] = tr_wait; pace[4u * E + i] = tr_fail;\n";
+    s << "  }\n";
+  }
+  s << "}\n";
+  }
   st.smem_per_warp = (2 * qmax * 1024 + T - 1) / T;
   return s.str();
 }

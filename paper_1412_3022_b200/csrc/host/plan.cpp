@@ -59,6 +59,14 @@ static std::string source_key(const std::string &src) {
 
 static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
   GenOptions oo = o;
+  if (oo.layout < 0) {
+    // group-specialised CTAs when the groups tile the 148 SMs with <= 10% left idle
+    GenStats g0;
+    oo.layout = 0;
+    (void)generate_source(p, oo, g0);
+    const int G = std::max(1, g0.groups), sms = 148;
+    oo.layout = (G <= sms && (sms % G) * 10 <= sms) ? 1 : 0;
+  }
   // warps per CTA from the shared-memory budget (2 stage buffers of in_block KiB per team)
   GenStats probe;
   (void)generate_source(p, oo, probe);
@@ -139,6 +147,8 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
   k.n_groups = std::max(1, k.stats.groups);
   k.tpb = oo.tpb;
   k.chunk_loop = oo.chunk_loop;
+  k.layout = oo.layout;
+  k.teams = std::max(1, oo.warps / std::max(1, oo.team));
   k.smem = (size_t)k.stats.smem_per_warp * oo.warps;
   std::vector<char> cubin;
   bool cached = false;
@@ -179,10 +189,22 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
   int sms = 148;
   D.DeviceGetAttribute(&sms, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev);
   k.sms = sms;
+  if (k.layout == 1 && (oo.pace_lag > 0 || oo.trace)) {
+    k.pace_entries = 4096;  // per field; 5 fields (progress, then trace: start, end, wait, timeouts)
+    if (cudaMalloc(&k.pace, k.pace_entries * 8 * 6) != cudaSuccess ||
+        cudaMemset(k.pace, 0, k.pace_entries * 8 * 6) != cudaSuccess) {
+      cudaGetLastError();
+      free_kernel(k);
+      err = "cudaMalloc(pace counters)";
+      return PMRC_ENOMEM;
+    }
+  }
   return PMRC_OK;
 }
 
 void free_kernel(Kernel &k) {
+  if (k.pace) cudaFree(k.pace);
+  k.pace = nullptr;
   if (k.module && drv().ok) drv().ModuleUnload((CUmodule)k.module);
   k.module = nullptr;
   k.function = nullptr;
@@ -205,11 +227,22 @@ int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides
       buf[k.n_slots + i] = strides[i];
     }
     uint64_t S64 = S;
-    void *args[] = {buf.data(), &S64, (void *)&ns, (void *)&chunks};
     // the kernel splits the ns * chunks chunk range evenly over the CTAs
     uint64_t grid = (uint64_t)k.sms * k.blocks_per_sm;
-    grid = std::min<uint64_t>(grid, (uint64_t)ns * chunks);
-    grid = std::max<uint64_t>(grid, 1);
+    if (k.layout == 1) {
+      // group-specialised: G groups x spg chunk ranges (grid must be a multiple of G)
+      const uint64_t G = (uint64_t)k.n_groups;
+      uint64_t spg = std::max<uint64_t>(1, grid / G);
+      spg = std::min<uint64_t>(spg, (uint64_t)ns * chunks);
+      grid = G * spg;
+    } else {
+      grid = std::min<uint64_t>(grid, (uint64_t)ns * chunks);
+      grid = std::max<uint64_t>(grid, 1);
+    }
+    // pacing only when every CTA has its counters and can be co-resident
+    void *pace = (k.pace && grid * k.teams <= k.pace_entries) ? k.pace : nullptr;
+    const uint32_t epoch = ++k.epoch;
+    void *args[] = {buf.data(), &S64, (void *)&ns, (void *)&chunks, &pace, (void *)&epoch};
     CUresult cr = drv().LaunchKernel((CUfunction)k.function, (unsigned)grid, 1, 1, k.tpb, 1, 1, (unsigned)k.smem, (CUstream)stream, args,
                                  nullptr);
     if (cr != CUDA_SUCCESS) { err = "cuLaunchKernel: " + cu_err(cr); return PMRC_ECUDA; }

@@ -46,7 +46,10 @@ struct GenOptions {
   int chunk_loop = 24;      // chunks per team per group (loop: instruction reuse)
   int team = 2;             // warps sharing one chunk's stage buffer (each computes 1/team of the rows)
   int ld_hint = 1;
-  bool fold = true;         // eager-fold emission of XOR networks (low register pressure)          // 0: __ldg/__stcs; 1: L2 evict-first cache-hinted loads/stores
+  bool fold = true;         // eager-fold emission of XOR networks (low register pressure)
+  int layout = -1;          // 0: every CTA walks all groups; 1: group-specialised CTAs; -1: auto
+  bool trace = false;       // layout 1 diagnostics: per-team start/end/wait times (pmrc_debug_counters)
+  int pace_lag = 0;         // layout 1: max chunks a team runs ahead of its peers (0 = no pacing)
 };
 
 struct GenStats {
@@ -70,6 +73,11 @@ struct Kernel {
   int n_groups = 0;
   int tpb = 256;
   int chunk_loop = 1;
+  int layout = 0;
+  int teams = 1;
+  void *pace = nullptr;             // layout 1: per-(CTA, team) progress counters (device)
+  size_t pace_entries = 0;
+  mutable uint32_t epoch = 0;       // launch epoch (counters carry it, so they never need a reset)
   size_t smem = 0;
   int blocks_per_sm = 1;
   int sms = 148;

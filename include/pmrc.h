@@ -148,6 +148,14 @@ int pmrc_precompile(const pmrc_code *c);
  * up to cap bytes (NUL-terminated if room) and the full length to *len. */
 int pmrc_encode_source(const pmrc_code *c, char *buf, size_t cap, size_t *len);
 
+/* The generated CUDA source of a decode (op 0: ids = survivors) or repair (op 1: lost_id, ids =
+ * helpers) plan, without a GPU and without launching; compile != 0 also NVRTC-compiles it into
+ * the kernel cache (so build() can pre-compile plans of known failure patterns).  Errors as
+ * pmrc_decode / pmrc_repair (e.g. PMRC_ESINGULAR); PMRC_EINVAL if the plan computes nothing
+ * (all data survives).  Output convention as pmrc_encode_source. */
+int pmrc_plan_source(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids, int compile, char *buf, size_t cap,
+                     size_t *len);
+
 /* Diagnostics of the encode kernel's CTA pacing (group-specialised layout): copies the device
  * counter area (5 x E u64: progress counters, then per-(CTA, team) start / end globaltimer ns, ns
  * spent pacing and pacing timeouts, the last four only with PMRC_GEN=trace=1) to host[0..cap) and

@@ -21,7 +21,7 @@ MATRIX_PSI, MATRIX_G, MATRIX_GSYS, MATRIX_GPP, MATRIX_LAMBDA = 0, 1, 2, 3, 4
 EXPORTS = ["pmrc_create", "pmrc_destroy", "pmrc_info", "pmrc_matrix", "pmrc_layout", "pmrc_encode",
            "pmrc_encode_host", "pmrc_decode", "pmrc_repair", "pmrc_repair_project", "pmrc_repair_combine",
            "pmrc_read_cost", "pmrc_launch_count", "pmrc_strerror", "pmrc_last_error", "pmrc_precompile",
-           "pmrc_encode_source", "pmrc_debug_counters"]
+           "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source"]
 
 
 class PmrcError(RuntimeError):
@@ -77,6 +77,7 @@ def lib():
             "pmrc_precompile": ([P], I),
             "pmrc_encode_source": ([P, P, Z, ctypes.POINTER(ctypes.c_size_t)], I),
             "pmrc_debug_counters": ([P, P, Z, ctypes.POINTER(ctypes.c_size_t)], I),
+            "pmrc_plan_source": ([P, I, I, IP, I, I, P, Z, ctypes.POINTER(ctypes.c_size_t)], I),
             "pmrc_strerror": ([I], ctypes.c_char_p),
             "pmrc_last_error": ([], ctypes.c_char_p),
         }
@@ -190,6 +191,18 @@ def pmrc_encode_source(code):
     _check(lib().pmrc_encode_source(code, None, 0, ctypes.byref(n)), "pmrc_encode_source")
     buf = ctypes.create_string_buffer(n.value + 1)
     _check(lib().pmrc_encode_source(code, buf, n.value + 1, ctypes.byref(n)), "pmrc_encode_source")
+    return buf.value.decode()
+
+
+def pmrc_plan_source(code, op, lost_id, ids, compile=False):
+    """Generated source of a decode (op 0, ids = survivors) or repair (op 1) plan; no GPU needed."""
+    n = ctypes.c_size_t(0)
+    arr, _ = _ints(ids)
+    _check(lib().pmrc_plan_source(code, op, lost_id, arr, len(ids), int(compile), None, 0, ctypes.byref(n)),
+           "pmrc_plan_source")
+    buf = ctypes.create_string_buffer(n.value + 1)
+    _check(lib().pmrc_plan_source(code, op, lost_id, arr, len(ids), 0, buf, n.value + 1, ctypes.byref(n)),
+           "pmrc_plan_source")
     return buf.value.decode()
 
 

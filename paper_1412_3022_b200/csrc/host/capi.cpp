@@ -46,6 +46,8 @@ struct pmrc_code {
   std::map<std::string, int> plan_err;                   // cached failures (ESINGULAR)
   std::map<std::string, int> plan_meta;                  // e.g. blocks written by a decode plan
   HostStage hs;
+  std::string *dry = nullptr;  // pmrc_plan_source: get_kernel stores the generated source here instead
+  bool dry_compile = false;    //   (and NVRTC-compiles it into the kernel cache if set)
 };
 
 namespace {
@@ -69,7 +71,19 @@ int ensure_device(pmrc_code *c) {
   return PMRC_OK;
 }
 
+constexpr int kDryRun = 1;  // internal: plan generated for pmrc_plan_source, nothing launched
+
 int get_kernel(pmrc_code *c, const std::string &key, const PlanSpec &spec, Kernel **out) {
+  if (c->dry) {
+    GenStats st;
+    *c->dry = plan_source(spec, c->gen, st);
+    if (c->dry_compile) {
+      std::string err;
+      int rc = precompile_kernel(spec, c->gen, err);
+      if (rc) return fail(rc, err);
+    }
+    return kDryRun;
+  }
   auto it = c->plans.find(key);
   if (it != c->plans.end()) {
     *out = it->second.get();
@@ -207,6 +221,8 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "layout") c->gen.layout = v;
         if (key == "pace_lag") c->gen.pace_lag = v;
         if (key == "trace") c->gen.trace = v != 0;
+        if (key == "net_in") c->gen.net_in = v;
+        if (key == "fence") c->gen.fence = v != 0;
       }
       pos = e + 1;
     }
@@ -288,10 +304,36 @@ int pmrc_debug_counters(const pmrc_code *c, unsigned long long *host, size_t cap
   return PMRC_OK;
 }
 
+int pmrc_plan_source(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids, int compile, char *buf, size_t cap,
+                     size_t *len) {
+  if (!c || !ids) return fail(PMRC_EINVAL, "NULL argument");
+  std::string src;
+  c->dry = &src;
+  c->dry_compile = compile != 0;
+  std::vector<pmrc_cregion> pieces(std::max(1, n_ids), pmrc_cregion{(const void *)(uintptr_t)4096, 0});
+  int rc;
+  if (op == 0) {
+    int nw = 0;
+    rc = pmrc_decode(c, ids, n_ids, pieces.data(), (void *)(uintptr_t)4096, 16, 0, &nw, nullptr);
+  } else {
+    rc = pmrc_repair(c, lost_id, ids, n_ids, pieces.data(), pmrc_region{(void *)(uintptr_t)4096, 0}, 16, 0, nullptr);
+  }
+  c->dry = nullptr;
+  c->dry_compile = false;
+  if (rc != kDryRun) return rc ? rc : fail(PMRC_EINVAL, "no kernel for this plan (nothing to compute)");
+  if (len) *len = src.size();
+  if (buf && cap) {
+    size_t n = std::min(cap - 1, src.size());
+    memcpy(buf, src.data(), n);
+    buf[n] = 0;
+  }
+  return PMRC_OK;
+}
+
 int pmrc_encode_source(const pmrc_code *c, char *buf, size_t cap, size_t *len) {
   if (!c) return fail(PMRC_EINVAL, "NULL handle");
   GenStats st;
-  std::string src = generate_source(c->enc_spec, c->gen, st);
+  std::string src = plan_source(c->enc_spec, c->gen, st);
   if (len) *len = src.size();
   if (buf && cap) {
     size_t n = std::min(cap - 1, src.size());

@@ -343,6 +343,48 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
       for (size_t j = i; j < std::min(kv.second.size(), i + (size_t)o.max_rows); j++) g.rows.push_back(kv.second[j]);
       groups.push_back(g);
     }
+  // Rows with (nearly) all-distinct supports (decode: rows of G~^-1) would make one group per row,
+  // each loading and transposing its own inputs.  Then cluster rows greedily instead: seed with the
+  // widest remaining row, add the rows that grow the union support least, up to max_rows; a zero
+  // coefficient inside a group's union costs a load but no XOR (skipped when the network is built).
+  const size_t min_groups = (R + o.max_rows - 1) / std::max(1, o.max_rows);
+  if (R > 0 && groups.size() > min_groups + min_groups / 2) {
+    std::vector<std::vector<char>> sup(R, std::vector<char>(C, 0));
+    std::vector<int> w(R, 0);
+    for (int r = 0; r < R; r++)
+      for (int c = 0; c < C; c++)
+        if (p.A.at(r, c)) sup[r][c] = 1, w[r]++;
+    std::vector<char> left(R, 1);
+    int nleft = R;
+    groups.clear();
+    while (nleft > 0) {
+      int seed = -1;
+      for (int r = 0; r < R; r++)
+        if (left[r] && (seed < 0 || w[r] > w[seed])) seed = r;
+      Group g;
+      std::vector<char> U = sup[seed];
+      g.rows.push_back(seed);
+      left[seed] = 0;
+      nleft--;
+      while ((int)g.rows.size() < o.max_rows && nleft > 0) {
+        int best = -1, bgrow = 1 << 30;
+        for (int r = 0; r < R; r++) {
+          if (!left[r]) continue;
+          int grow = 0;
+          for (int c = 0; c < C; c++) grow += sup[r][c] && !U[c];
+          if (grow < bgrow) { bgrow = grow; best = r; }
+        }
+        g.rows.push_back(best);
+        left[best] = 0;
+        nleft--;
+        for (int c = 0; c < C; c++) U[c] |= sup[best][c];
+      }
+      std::sort(g.rows.begin(), g.rows.end());
+      for (int c = 0; c < C; c++)
+        if (U[c]) g.cols.push_back(c);
+      groups.push_back(g);
+    }
+  }
   st.groups = (int)groups.size();
 
   // ---- stages: each group's inputs packed into shared-memory buffers of <= IB loaded blocks ----
@@ -571,10 +613,26 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
                 for (int bp = 0; bp < 8; bp++)
                   if ((br[b] >> bp) & 1) rows[r * 8 + b].push_back((int)ci * 8 + bp);
             }
-          Slp sl = make_slp((int)base.size(), rows, o.cse);
-          st.xor2 += sl.xor2() + (first ? 0 : 8 * m);
+          // the stage's network, optionally cut into sub-networks over net_in inputs each (CSE
+          // within a sub-network only): temps and plane quads then die at sub-network boundaries,
+          // which bounds register pressure for wide plans (decode) at the price of some sharing
+          const int ncols = (int)sg.cols.size();
+          const int sub = o.net_in > 0 ? o.net_in : ncols;
+          std::vector<Slp> subs;
+          std::vector<std::vector<std::string>> sub_base;
+          for (int c0 = 0; c0 < ncols; c0 += sub) {
+            const int c1 = std::min(ncols, c0 + sub);
+            std::vector<std::vector<int>> sr(rows.size());
+            for (size_t r = 0; r < rows.size(); r++)
+              for (int x : rows[r])
+                if (x >= 8 * c0 && x < 8 * c1) sr[r].push_back(x - 8 * c0);
+            subs.push_back(make_slp(8 * (c1 - c0), sr, o.cse));
+            sub_base.emplace_back(base.begin() + 8 * c0, base.begin() + 8 * c1);
+            const bool acc = !(first && c0 == 0);
+            st.xor2 += subs.back().xor2() + (acc ? 8 * m : 0);
+            st.xor2_naive += make_slp(8 * (c1 - c0), sr, false).xor2() + (acc ? 8 * m : 0);
+          }
           st.naive_lop3 += naive_lop3(rows);
-          st.xor2_naive += make_slp((int)base.size(), rows, false).xor2() + (first ? 0 : 8 * m);
           std::vector<char> loaded(2 * nblk, 0);
           std::ostringstream net;
           auto need = [&](const std::string &nmb) {
@@ -587,10 +645,26 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
           for (int h = 0; h < 2 * nblk; h++)
             if (used_half[h] && !loaded[h]) need("P" + std::to_string(h) + ".x");
           net << body.str();
-          if (o.fold)
-            emit_slp_fold(net, sl, base, outs, !first, "t", need);
-          else
-            emit_slp_lazy(net, sl, base, outs, !first, "t", need);
+          for (size_t si2 = 0; si2 < subs.size(); si2++) {
+            const bool acc = !(first && si2 == 0);
+            const std::string tp = subs.size() > 1 ? "t" + std::to_string(si2) + "_" : "t";
+            if (subs.size() > 1) net << "          {\n";
+            if (o.fold)
+              emit_slp_fold(net, subs[si2], sub_base[si2], outs, acc, tp, need);
+            else
+              emit_slp_lazy(net, subs[si2], sub_base[si2], outs, acc, tp, need);
+            if (subs.size() > 1) net << "          }\n";
+            if (o.fence) {
+              // register fence: the accumulators pass through an empty volatile asm, so ptxas
+              // cannot interleave (and keep live together) the networks of consecutive stages
+              for (size_t f0 = 0; f0 < outs.size(); f0 += 8) {
+                net << "          asm volatile(\"\" :";
+                for (size_t f = f0; f < std::min(outs.size(), f0 + 8); f++)
+                  net << (f > f0 ? ", " : " ") << "\"+r\"(" << outs[f] << ")";
+                net << ");\n";
+              }
+            }
+          }
           s << net.str();
           first = false;
         }
@@ -762,6 +836,7 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
   s << "}\n";
   }
   st.smem_per_warp = (2 * qmax * 1024 + T - 1) / T;
+  for (auto &gs : gstages) st.max_stages = std::max(st.max_stages, (int)gs.size());
   return s.str();
 }
 

@@ -72,7 +72,11 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
   (void)generate_source(p, oo, probe);
   int budget = 220 * 1024;
   int w = std::max(1, std::min(16, budget / std::max(1, probe.smem_per_warp)));
-  if (o.warps > 0) w = std::min(w, o.warps);
+  // measured (profiles/r01b): 12 warps for single-stage groups (encode); 8 for wide multi-stage
+  // groups (decode: 4 stages of 14 inputs), where fewer, larger-register warps schedule better
+  int want = o.warps;
+  if (want <= 0) want = probe.max_stages >= 3 ? 8 : 12;
+  w = std::min(w, want);
   w = std::max(oo.team, w - w % std::max(1, oo.team));  // whole teams
   oo.warps = w;
   oo.tpb = 32 * oo.warps;
@@ -129,6 +133,10 @@ static int compile_cubin(const std::string &src, std::vector<char> &cubin, bool 
   return PMRC_OK;
 }
 
+std::string plan_source(const PlanSpec &p, const GenOptions &o, GenStats &st) {
+  return generate_source(p, resolve_options(p, o), st);
+}
+
 int precompile_kernel(const PlanSpec &p, const GenOptions &o, std::string &err) {
   GenOptions oo = resolve_options(p, o);
   GenStats st;
@@ -143,6 +151,9 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
   k = Kernel();
   GenOptions oo = resolve_options(p, o);
   k.source = generate_source(p, oo, k.stats);
+  if (const char *dd = getenv("PMRC_DUMP")) {  // diagnostics: keep the generated source of every plan
+    std::ofstream(std::string(dd) + "/" + source_key(k.source) + ".cu") << k.source;
+  }
   k.n_slots = std::max(1, p.n_slots);
   k.n_groups = std::max(1, k.stats.groups);
   k.tpb = oo.tpb;

@@ -38,7 +38,7 @@ struct PlanSpec {
 struct GenOptions {
   int max_rows = 8;      // output blocks per group (8 planes each in registers)
   int in_block = 14;     // loaded blocks per stage (shared-memory buffer of in_block KiB, x2)
-  int warps = 12;        // warps per CTA (capped by the 220 KiB shared-memory budget)
+  int warps = 0;         // warps per CTA (0 = auto: 12, or 8 for plans of >= 3 stages per group; capped by smem)
   int tpb = 256;         // (derived) threads per CTA
   bool cse = true;       // Paar CSE (false: naive per-row XOR chains)
   bool sync_groups = true;  // __syncthreads() before each group: warps of a CTA execute the same code
@@ -48,6 +48,8 @@ struct GenOptions {
   int ld_hint = 1;
   bool fold = true;         // eager-fold emission of XOR networks (low register pressure)
   int layout = -1;          // 0: every CTA walks all groups; 1: group-specialised CTAs; -1: auto
+  bool fence = true;        // register fence after every (sub-)network (see codegen.cpp)
+  int net_in = 7;           // inputs per CSE sub-network within a stage (0 = the whole stage)
   bool trace = false;       // layout 1 diagnostics: per-team start/end/wait times (pmrc_debug_counters)
   int pace_lag = 0;         // layout 1: max chunks a team runs ahead of its peers (0 = no pacing)
 };
@@ -60,6 +62,7 @@ struct GenStats {
   int transposes = 0;    // 8x8 bit transposes per 32 byte positions (in + out)
   long loads = 0;        // 16-B vector loads per lane per item sum
   int smem_per_warp = 0; // bytes of shared memory (transposed input planes) per warp
+  int max_stages = 0;    // most shared-memory stages of any group
 };
 
 // Generate CUDA C++ source of the bitsliced kernel `pmrc_kernel` for a plan.
@@ -91,6 +94,8 @@ struct Kernel {
 // Generate + NVRTC-compile + load.  Returns 0 or PMRC_E*; err gets the log on failure.
 int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string &err);
 void free_kernel(Kernel &k);
+// Source of the kernel build_kernel would compile (options resolved).
+std::string plan_source(const PlanSpec &p, const GenOptions &o, GenStats &st);
 // Generate + NVRTC-compile into the kernel cache only (no GPU needed).
 int precompile_kernel(const PlanSpec &p, const GenOptions &o, std::string &err);
 

@@ -223,6 +223,9 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "trace") c->gen.trace = v != 0;
         if (key == "net_in") c->gen.net_in = v;
         if (key == "fence") c->gen.fence = v != 0;
+        if (key == "tr_unroll" && v > 0) c->gen.tr_unroll = v;
+        if (key == "sched") c->gen.sched = v != 0;
+        if (key == "grid_ctas" && v > 0) c->gen.grid_ctas = v;
       }
       pos = e + 1;
     }

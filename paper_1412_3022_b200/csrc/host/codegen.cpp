@@ -295,6 +295,113 @@ void emit_slp_fold(std::ostringstream &s, const Slp &p, const std::vector<std::s
   }
 }
 
+// Register-pressure-aware eager-fold emission: the same fold mechanics as emit_slp_fold, but the
+// next temp is chosen greedily (instead of in CSE creation order) to minimise the growth of live
+// values: loading a plane quad costs 4 registers, a new temp 1, and every operand (temp or quad)
+// whose last consumer this temp is frees its registers.  Ties: CSE order.
+template <class Need>
+void emit_slp_sched(std::ostringstream &s, const Slp &p, const std::vector<std::string> &base,
+                    const std::vector<std::string> &outs, bool accumulate, const std::string &tpref, Need need) {
+  const int nin = p.n_in, nt = (int)p.tmp.size(), nr = (int)p.rows.size();
+  const int nq = (nin + 3) / 4;
+  std::vector<std::vector<int>> rows_of(nin + nt), tmps_of(nin + nt);
+  for (int r = 0; r < nr; r++)
+    for (int x : p.rows[r]) rows_of[x].push_back(r);
+  for (int i = 0; i < nt; i++)
+    for (int x : p.tmp[i]) tmps_of[x].push_back(i);
+  // remaining temp consumers of each signal, and of each quad (sum over its planes)
+  std::vector<int> tleft(nin + nt, 0), qleft(nq, 0);
+  for (int i = 0; i < nt; i++)
+    for (int x : p.tmp[i]) {
+      tleft[x]++;
+      if (x < nin) qleft[x / 4]++;
+    }
+  std::vector<std::vector<int>> pending(nr);
+  std::vector<char> started(nr, accumulate ? 1 : 0), quad_done(nq, 0), made(nt, 0);
+  auto name = [&](int sig) { return sig < nin ? base[sig] : tpref + std::to_string(sig - nin); };
+  auto try_fold = [&](int r) {
+    auto &pd = pending[r];
+    if (!started[r]) {
+      if (pd.size() < 3) return;
+      s << "    " << outs[r] << " = " << name(pd[0]) << " ^ " << name(pd[1]) << " ^ " << name(pd[2]) << ";\n";
+      pd.erase(pd.begin(), pd.begin() + 3);
+      started[r] = 1;
+    }
+    while (pd.size() >= 2) {
+      s << "    " << outs[r] << " ^= " << name(pd[0]) << " ^ " << name(pd[1]) << ";\n";
+      pd.erase(pd.begin(), pd.begin() + 2);
+    }
+  };
+  auto make_available = [&](int sig) {
+    for (int r : rows_of[sig]) {
+      pending[r].push_back(sig);
+      try_fold(r);
+    }
+  };
+  auto load_quad = [&](int q) {
+    if (quad_done[q]) return;
+    quad_done[q] = 1;
+    need(base[4 * q]);
+    for (int x = 4 * q; x < std::min(nin, 4 * q + 4); x++) make_available(x);
+  };
+  for (int step = 0; step < nt; step++) {
+    int best = -1, bscore = 1 << 30;
+    for (int i = 0; i < nt; i++) {
+      if (made[i]) continue;
+      bool ready = true;
+      for (int x : p.tmp[i])
+        if (x >= nin && !made[x - nin]) ready = false;
+      if (!ready) continue;
+      int sc = 1;
+      int qs[3] = {-1, -1, -1}, nqs = 0;
+      for (int x : p.tmp[i]) {
+        if (x >= nin) {
+          if (tleft[x] == 1) sc -= 1;
+        } else {
+          const int q = x / 4;
+          bool seen = false;
+          for (int k = 0; k < nqs; k++) seen |= qs[k] == q;
+          if (seen) continue;
+          qs[nqs++] = q;
+          int use = 0;
+          for (int y : p.tmp[i])
+            if (y < nin && y / 4 == q) use++;
+          if (!quad_done[q]) sc += 4;
+          if (qleft[q] == use) sc -= 4;
+        }
+      }
+      if (sc < bscore) { bscore = sc; best = i; }
+    }
+    const int i = best;
+    for (int x : p.tmp[i])
+      if (x < nin) load_quad(x / 4);
+    s << "    const u32 " << tpref << i << " = ";
+    for (size_t j = 0; j < p.tmp[i].size(); j++) s << (j ? " ^ " : "") << name(p.tmp[i][j]);
+    s << ";\n";
+    made[i] = 1;
+    for (int x : p.tmp[i]) {
+      tleft[x]--;
+      if (x < nin) qleft[x / 4]--;
+    }
+    make_available(nin + i);
+  }
+  for (int r = 0; r < nr; r++)
+    for (int x : p.rows[r])
+      if (x < nin) load_quad(x / 4);
+  for (int r = 0; r < nr; r++) {
+    auto &pd = pending[r];
+    if (!started[r]) {
+      s << "    " << outs[r] << " = ";
+      if (pd.empty()) s << "0u";
+      for (size_t j = 0; j < pd.size(); j++) s << (j ? " ^ " : "") << name(pd[j]);
+      s << ";\n";
+    } else if (!pd.empty()) {
+      s << "    " << outs[r] << " ^= " << name(pd[0]) << ";\n";
+    }
+    pd.clear();
+  }
+}
+
 void emit_slp(std::ostringstream &s, const Slp &p, const std::vector<std::string> &base,
               const std::vector<std::string> &outs, bool accumulate, const std::string &tpref) {
   emit_slp_lazy(s, p, base, outs, accumulate, tpref, [](const std::string &) {});
@@ -386,6 +493,16 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     }
   }
   st.groups = (int)groups.size();
+  {
+    long mn = 1L << 40, mx = 0;
+    for (auto &g : groups) {
+      long c = (long)g.rows.size();
+      for (int col : g.cols) c += (long)p.inputs[col].terms.size();
+      mn = std::min(mn, c);
+      mx = std::max(mx, c);
+    }
+    st.group_cost_ratio = groups.empty() ? 1.0 : (double)mx / (double)std::max(1L, mn);
+  }
 
   // ---- stages: each group's inputs packed into shared-memory buffers of <= IB loaded blocks ----
   const int IB = std::max(1, o.in_block);
@@ -470,11 +587,10 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   if (!L) s << "0u";
   s << "};\n";
 
-  s << R"CUDA(
-// in-place 8x8 bit transpose of this lane's 32 bytes of blocks [lo, hi) of a stage buffer
-static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 lo, const u32 hi) {
-  #pragma unroll 1
-  for (u32 i = lo; i < hi; i++) {
+  s << "\n// in-place 8x8 bit transpose of this lane's 32 bytes of blocks [lo, hi) of a stage buffer\n"
+       "static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 lo, const u32 hi) {\n"
+       "  #pragma unroll " << std::max(1, o.tr_unroll) << "\n";
+  s << R"CUDA(  for (u32 i = lo; i < hi; i++) {
     const u32 a0 = buf + i * 1024u, a1 = a0 + 512u;
     const uint4 a = pm_lds(a0), b = pm_lds(a1);
     u32 w0 = a.x, w1 = a.y, w2 = a.z, w3 = a.w, w4 = b.x, w5 = b.y, w6 = b.z, w7 = b.w;
@@ -520,6 +636,54 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
     o2 << ind << "  default: break;\n" << ind << "  }\n" << ind << "}\n";
   };
 
+  if (o.layout == 2) {
+    // layout 2: groups of unequal cost (MBR: d- and k-input groups) get CTAs in proportion to
+    // their estimated instruction count, from a table for a grid of PM_NG CTAs (plan.cpp)
+    std::vector<double> w(groups.size());
+    double tot = 0;
+    for (size_t g = 0; g < groups.size(); g++) {
+      long ones = 0;
+      for (int r : groups[g].rows)
+        for (int c : groups[g].cols)
+          if (uint8_t cf = p.A.at(r, c)) {
+            uint8_t br[8];
+            coef_rows(cf, br);
+            for (int b = 0; b < 8; b++) ones += __builtin_popcount(br[b]);
+          }
+      long nblk = 0;
+      for (int c : groups[g].cols) nblk += (long)p.inputs[c].terms.size();
+      w[g] = 48.0 * (double)(nblk + (long)groups[g].rows.size()) + 0.3 * (double)ones + 150.0;
+      tot += w[g];
+    }
+    const int NG = std::max<int>((int)groups.size(), o.grid_ctas);
+    std::vector<int> n(groups.size(), 1);
+    int used = (int)groups.size();
+    // largest-remainder apportionment of the remaining CTAs
+    std::vector<double> want(groups.size());
+    for (size_t g = 0; g < groups.size(); g++) want[g] = NG * w[g] / tot;
+    while (used < NG) {
+      size_t bg = 0;
+      double bd = -1e30;
+      for (size_t g = 0; g < groups.size(); g++) {
+        const double d = want[g] - n[g];
+        if (d > bd) { bd = d; bg = g; }
+      }
+      n[bg]++;
+      used++;
+    }
+    s << "#define PM_NG " << NG << "u\n";
+    std::ostringstream tg, tr, tn;
+    int k = 0;
+    for (size_t g = 0; g < groups.size(); g++)
+      for (int r = 0; r < n[g]; r++, k++) {
+        tg << (k ? ", " : "") << g;
+        tr << (k ? ", " : "") << r;
+        tn << (k ? ", " : "") << n[g];
+      }
+    s << "__constant__ unsigned short pm_cta_g[" << NG << "] = {" << tg.str() << "};\n";
+    s << "__constant__ unsigned short pm_cta_r[" << NG << "] = {" << tr.str() << "};\n";
+    s << "__constant__ unsigned short pm_cta_n[" << NG << "] = {" << tn.str() << "};\n";
+  }
   const int TPB = 32 * std::max(T, o.warps);
   const int teams = TPB / 32 / T;
   s << "extern \"C\" __global__ void __launch_bounds__(" << TPB << ", 1) pmrc_kernel(const __grid_constant__ Slots R, "
@@ -649,7 +813,9 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
             const bool acc = !(first && si2 == 0);
             const std::string tp = subs.size() > 1 ? "t" + std::to_string(si2) + "_" : "t";
             if (subs.size() > 1) net << "          {\n";
-            if (o.fold)
+            if (o.fold && o.sched)
+              emit_slp_sched(net, subs[si2], sub_base[si2], outs, acc, tp, need);
+            else if (o.fold)
               emit_slp_fold(net, subs[si2], sub_base[si2], outs, acc, tp, need);
             else
               emit_slp_lazy(net, subs[si2], sub_base[si2], outs, acc, tp, need);
@@ -758,7 +924,12 @@ static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 
   // second read hits L2) and each SM only ever executes one group's code (instruction cache).
   // Teams interleave over the range (team, team + teams, ...) so all groups advance in step.
   s << "  const u32 teams = " << teams << "u;\n";
-  s << "  const u32 spg = gridDim.x / " << groups.size() << "u, g = blockIdx.x / spg, r = blockIdx.x - g * spg;\n";
+  if (o.layout == 2) {
+    s << "  if (blockIdx.x >= PM_NG) return;\n";
+    s << "  const u32 g = pm_cta_g[blockIdx.x], r = pm_cta_r[blockIdx.x], spg = pm_cta_n[blockIdx.x];\n";
+  } else {
+    s << "  const u32 spg = gridDim.x / " << groups.size() << "u, g = blockIdx.x / spg, r = blockIdx.x - g * spg;\n";
+  }
   s << "  const u32 total = stripes * chunks;\n";
   s << "  const u32 c0 = (u32)((u64)total * r / spg), c1 = (u32)((u64)total * (r + 1u) / spg);\n";
   s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (2u * PM_QMAX * 1024u);\n";

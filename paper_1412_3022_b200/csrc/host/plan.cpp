@@ -66,6 +66,7 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     (void)generate_source(p, oo, g0);
     const int G = std::max(1, g0.groups), sms = 148;
     oo.layout = (G <= sms && (sms % G) * 10 <= sms) ? 1 : 0;
+    if (oo.layout == 1 && g0.group_cost_ratio > 1.2) oo.layout = 2;  // unequal groups: apportion CTAs
   }
   // warps per CTA from the shared-memory budget (2 stage buffers of in_block KiB per team)
   GenStats probe;
@@ -159,6 +160,7 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
   k.tpb = oo.tpb;
   k.chunk_loop = oo.chunk_loop;
   k.layout = oo.layout;
+  k.grid_ctas = oo.grid_ctas;
   k.teams = std::max(1, oo.warps / std::max(1, oo.team));
   k.smem = (size_t)k.stats.smem_per_warp * oo.warps;
   std::vector<char> cubin;
@@ -221,6 +223,8 @@ void free_kernel(Kernel &k) {
   k.function = nullptr;
 }
 
+static int oo_grid(const Kernel &k) { return k.grid_ctas; }
+
 int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides, size_t S, size_t stripes,
                   void *stream, std::string &err) {
   if (S == 0 || stripes == 0) return PMRC_OK;
@@ -240,7 +244,9 @@ int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides
     uint64_t S64 = S;
     // the kernel splits the ns * chunks chunk range evenly over the CTAs
     uint64_t grid = (uint64_t)k.sms * k.blocks_per_sm;
-    if (k.layout == 1) {
+    if (k.layout == 2) {
+      grid = (uint64_t)std::max(k.n_groups, oo_grid(k));
+    } else if (k.layout == 1) {
       // group-specialised: G groups x spg chunk ranges (grid must be a multiple of G)
       const uint64_t G = (uint64_t)k.n_groups;
       uint64_t spg = std::max<uint64_t>(1, grid / G);

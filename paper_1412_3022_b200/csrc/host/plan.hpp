@@ -47,7 +47,11 @@ struct GenOptions {
   int team = 2;             // warps sharing one chunk's stage buffer (each computes 1/team of the rows)
   int ld_hint = 1;
   bool fold = true;         // eager-fold emission of XOR networks (low register pressure)
-  int layout = -1;          // 0: every CTA walks all groups; 1: group-specialised CTAs; -1: auto
+  int layout = -1;          // 0: every CTA walks all groups; 1: group-specialised CTAs; 2: same, CTAs
+                            // apportioned by group cost; -1: auto
+  int grid_ctas = 148;      // layout 2: CTAs the apportionment table is made for (one per SM)
+  bool sched = false;       // register-pressure-aware temp order (emit_slp_sched) instead of CSE order
+  int tr_unroll = 1;        // unroll factor of the in-place input transpose loop
   bool fence = true;        // register fence after every (sub-)network (see codegen.cpp)
   int net_in = 7;           // inputs per CSE sub-network within a stage (0 = the whole stage)
   bool trace = false;       // layout 1 diagnostics: per-team start/end/wait times (pmrc_debug_counters)
@@ -63,6 +67,7 @@ struct GenStats {
   long loads = 0;        // 16-B vector loads per lane per item sum
   int smem_per_warp = 0; // bytes of shared memory (transposed input planes) per warp
   int max_stages = 0;    // most shared-memory stages of any group
+  double group_cost_ratio = 1;  // max / min estimated group cost (loaded blocks + outputs)
 };
 
 // Generate CUDA C++ source of the bitsliced kernel `pmrc_kernel` for a plan.
@@ -77,6 +82,7 @@ struct Kernel {
   int tpb = 256;
   int chunk_loop = 1;
   int layout = 0;
+  int grid_ctas = 148;
   int teams = 1;
   void *pace = nullptr;             // layout 1: per-(CTA, team) progress counters (device)
   size_t pace_entries = 0;

@@ -156,6 +156,19 @@ int pmrc_encode_source(const pmrc_code *c, char *buf, size_t cap, size_t *len);
 int pmrc_plan_source(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids, int compile, char *buf, size_t cap,
                      size_t *len);
 
+/* Work of a plan (op 0 decode, 1 repair as in pmrc_plan_source; op 2 encode, ids ignored), per
+ * stripe and per 32 byte positions of every block, for roofline accounting:
+ * in_blocks / out_blocks = distinct blocks read / written per stripe (algorithmic HBM bytes =
+ * (in_blocks + out_blocks) * S per stripe); naive_lop3 = SURVEY §8(d)'s W (3-input XORs of the
+ * GF(2) expansion with zero coefficients skipped); xor2 = 2-input XORs of the emitted networks;
+ * transposes = 8x8 bit transposes (24 LOP3 each).  No GPU needed. */
+typedef struct {
+  int groups, in_blocks, out_blocks;
+  long long naive_lop3, xor2;
+  int transposes;
+} pmrc_plan_stats_t;
+int pmrc_plan_stats(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids, pmrc_plan_stats_t *out);
+
 /* Diagnostics of the encode kernel's CTA pacing (group-specialised layout): copies the device
  * counter area (5 x E u64: progress counters, then per-(CTA, team) start / end globaltimer ns, ns
  * spent pacing and pacing timeouts, the last four only with PMRC_GEN=trace=1) to host[0..cap) and

@@ -21,7 +21,7 @@ MATRIX_PSI, MATRIX_G, MATRIX_GSYS, MATRIX_GPP, MATRIX_LAMBDA = 0, 1, 2, 3, 4
 EXPORTS = ["pmrc_create", "pmrc_destroy", "pmrc_info", "pmrc_matrix", "pmrc_layout", "pmrc_encode",
            "pmrc_encode_host", "pmrc_decode", "pmrc_repair", "pmrc_repair_project", "pmrc_repair_combine",
            "pmrc_read_cost", "pmrc_launch_count", "pmrc_strerror", "pmrc_last_error", "pmrc_precompile",
-           "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source"]
+           "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source", "pmrc_plan_stats"]
 
 
 class PmrcError(RuntimeError):
@@ -46,6 +46,11 @@ class pmrc_info_t(ctypes.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class pmrc_plan_stats_t(ctypes.Structure):
+    _fields_ = [("groups", ctypes.c_int), ("in_blocks", ctypes.c_int), ("out_blocks", ctypes.c_int),
+                ("naive_lop3", ctypes.c_longlong), ("xor2", ctypes.c_longlong), ("transposes", ctypes.c_int)]
 
 
 _L = None
@@ -78,6 +83,7 @@ def lib():
             "pmrc_encode_source": ([P, P, Z, ctypes.POINTER(ctypes.c_size_t)], I),
             "pmrc_debug_counters": ([P, P, Z, ctypes.POINTER(ctypes.c_size_t)], I),
             "pmrc_plan_source": ([P, I, I, IP, I, I, P, Z, ctypes.POINTER(ctypes.c_size_t)], I),
+            "pmrc_plan_stats": ([P, I, I, IP, I, ctypes.POINTER(pmrc_plan_stats_t)], I),
             "pmrc_strerror": ([I], ctypes.c_char_p),
             "pmrc_last_error": ([], ctypes.c_char_p),
         }
@@ -204,6 +210,14 @@ def pmrc_plan_source(code, op, lost_id, ids, compile=False):
     _check(lib().pmrc_plan_source(code, op, lost_id, arr, len(ids), 0, buf, n.value + 1, ctypes.byref(n)),
            "pmrc_plan_source")
     return buf.value.decode()
+
+
+def pmrc_plan_stats(code, op, lost_id=0, ids=()):
+    """Per-stripe work of a decode (op 0) / repair (op 1) / encode (op 2) plan (roofline accounting)."""
+    st = pmrc_plan_stats_t()
+    arr, n = _ints(ids)
+    _check(lib().pmrc_plan_stats(code, op, lost_id, arr, n, ctypes.byref(st)), "pmrc_plan_stats")
+    return {f: getattr(st, f) for f, _ in pmrc_plan_stats_t._fields_}
 
 
 def pmrc_debug_counters(code):

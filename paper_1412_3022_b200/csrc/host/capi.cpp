@@ -47,6 +47,8 @@ struct pmrc_code {
   std::map<std::string, int> plan_meta;                  // e.g. blocks written by a decode plan
   HostStage hs;
   std::string *dry = nullptr;  // pmrc_plan_source: get_kernel stores the generated source here instead
+  PlanSpec dry_spec;           //   and the plan
+  GenStats dry_stats;
   bool dry_compile = false;    //   (and NVRTC-compiles it into the kernel cache if set)
 };
 
@@ -77,6 +79,8 @@ int get_kernel(pmrc_code *c, const std::string &key, const PlanSpec &spec, Kerne
   if (c->dry) {
     GenStats st;
     *c->dry = plan_source(spec, c->gen, st);
+    c->dry_spec = spec;
+    c->dry_stats = st;
     if (c->dry_compile) {
       std::string err;
       int rc = precompile_kernel(spec, c->gen, err);
@@ -333,6 +337,34 @@ int pmrc_plan_source(pmrc_code *c, int op, int lost_id, const int *ids, int n_id
   return PMRC_OK;
 }
 
+int pmrc_plan_stats(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids, pmrc_plan_stats_t *out) {
+  if (!c || !out) return fail(PMRC_EINVAL, "NULL argument");
+  memset(out, 0, sizeof(*out));
+  GenStats st;
+  PlanSpec spec;
+  if (op == 2) {
+    (void)plan_source(c->enc_spec, c->gen, st);
+    spec = c->enc_spec;
+  } else {
+    int rc = pmrc_plan_source(c, op, lost_id, ids, n_ids, 0, nullptr, 0, nullptr);
+    if (rc) return rc;
+    st = c->dry_stats;
+    spec = c->dry_spec;
+  }
+  std::vector<std::pair<int, int>> blocks;
+  for (auto &in : spec.inputs)
+    for (auto &t : in.terms) blocks.push_back({t.slot, t.blk});
+  std::sort(blocks.begin(), blocks.end());
+  blocks.erase(std::unique(blocks.begin(), blocks.end()), blocks.end());
+  out->groups = st.groups;
+  out->in_blocks = (int)blocks.size();
+  out->out_blocks = (int)spec.outputs.size();
+  out->naive_lop3 = st.naive_lop3;
+  out->xor2 = st.xor2;
+  out->transposes = st.transposes;
+  return PMRC_OK;
+}
+
 int pmrc_encode_source(const pmrc_code *c, char *buf, size_t cap, size_t *len) {
   if (!c) return fail(PMRC_EINVAL, "NULL handle");
   GenStats st;
@@ -460,7 +492,7 @@ int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregio
   const std::string key = ids_key("dec", surv_ids, n_surv, 0);
   auto fe = c->plan_err.find(key);
   if (fe != c->plan_err.end()) return fail(fe->second, "survivors do not span the data (cached)");
-  if (!c->plan_meta.count(key)) {
+  if (c->dry || !c->plan_meta.count(key)) {
     PlanSpec spec;
     {
       // ---- plan (R13): greedy B independent rows of G', systematic survivors first ----
@@ -594,7 +626,7 @@ int pmrc_repair(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers,
   auto fe = c->plan_err.find(key);
   if (fe != c->plan_err.end()) return fail(fe->second, "helper matrix singular (cached)");
   Kernel *K = nullptr;
-  if (!c->plans.count(key)) {
+  if (c->dry || !c->plans.count(key)) {
     Mat R;
     if (!repair_matrix(D, lost_id, helper_ids, R)) {
       c->plan_err[key] = PMRC_ESINGULAR;
@@ -685,7 +717,7 @@ int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids, int n_
   auto fe = c->plan_err.find(key);
   if (fe != c->plan_err.end()) return fail(fe->second, "helper matrix singular (cached)");
   Kernel *K = nullptr;
-  if (!c->plans.count(key)) {
+  if (c->dry || !c->plans.count(key)) {
     Mat R;
     if (!repair_matrix(D, lost_id, helper_ids, R)) {
       c->plan_err[key] = PMRC_ESINGULAR;

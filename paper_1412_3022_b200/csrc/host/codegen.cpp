@@ -854,7 +854,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         s << "        { unsigned char *pp = (unsigned char *)(ob" << od.slot << " + (u64)" << od.blk << "u * S);\n";
         s << "          pm_st(pp + o0, v0, " << n << "_0, " << n << "_1, " << n << "_2, " << n << "_3, pol_ef);\n";
         s << "          pm_st(pp + o1, v1, " << n << "_4, " << n << "_5, " << n << "_6, " << n << "_7, pol_ef); }\n";
-        if (rk == 0) st.transposes++;
+        st.transposes++;
       }
       s << "      } break;\n";
     }

@@ -106,3 +106,28 @@ def test_no_silent_cpu_fallback():
         assert e.value.rc == pm.PMRC_ECUDA
     finally:
         pm.pmrc_destroy(c)
+
+
+def test_plan_stats_and_source_without_gpu():
+    # plan generation is host-only: the per-stripe work of the config-2 plans
+    c = pm.pmrc_create(pm.PMRC_MSR_SPARSE, 8, 14, 16)
+    try:
+        enc = pm.pmrc_plan_stats(c, 2)
+        assert (enc["groups"], enc["in_blocks"], enc["out_blocks"], enc["naive_lop3"]) == (7, 56, 56, 12584)
+        assert enc["transposes"] == 7 * (14 + 8)          # every group: its 14 inputs + 8 outputs
+        dec = pm.pmrc_plan_stats(c, 0, 0, list(range(4, 12)))
+        assert dec["out_blocks"] == 4 * 7 and dec["in_blocks"] == 56   # nodes 0..3 lost
+        rep_par = pm.pmrc_plan_stats(c, 1, 15, [i for i in range(16) if i not in (15, 10)])
+        assert (rep_par["in_blocks"], rep_par["out_blocks"]) == (14 * 7, 7)     # f >= alpha: alpha blocks each
+        rep_sys = pm.pmrc_plan_stats(c, 1, 2, [i for i in range(16) if i not in (2, 12)])
+        assert (rep_sys["in_blocks"], rep_sys["out_blocks"]) == (14, 7)          # f < alpha: 1 block each
+        with pytest.raises(pm.PmrcError) as e:                                    # R10 singular set
+            pm.pmrc_plan_stats(c, 1, 0, [i for i in range(16) if i not in (0, 1)])
+        assert e.value.rc == pm.PMRC_ESINGULAR
+        with pytest.raises(pm.PmrcError) as e:                                    # all data survives
+            pm.pmrc_plan_stats(c, 0, 0, list(range(8)))
+        assert e.value.rc == pm.PMRC_EINVAL
+        src = pm.pmrc_plan_source(c, 1, 15, [i for i in range(16) if i not in (15, 10)])
+        assert "pmrc_kernel" in src and "lop3" in src
+    finally:
+        pm.pmrc_destroy(c)

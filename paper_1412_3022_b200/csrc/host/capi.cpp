@@ -229,6 +229,8 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "fence") c->gen.fence = v != 0;
         if (key == "tr_unroll" && v > 0) c->gen.tr_unroll = v;
         if (key == "sched") c->gen.sched = v != 0;
+        if (key == "cse_restarts" && v > 0) c->gen.cse_restarts = v;
+        if (key == "auto_wide") c->gen.auto_wide = v != 0;
         if (key == "grid_ctas" && v > 0) c->gen.grid_ctas = v;
       }
       pos = e + 1;

@@ -407,8 +407,19 @@ void emit_slp(std::ostringstream &s, const Slp &p, const std::vector<std::string
   emit_slp_lazy(s, p, base, outs, accumulate, tpref, [](const std::string &) {});
 }
 
+int g_cse_restarts = 1;  // set from GenOptions by generate_source
+
 Slp make_slp(int n_in, const std::vector<std::vector<int>> &rows, bool cse) {
-  if (cse) return cse3(n_in, rows);
+  if (cse) {
+    Slp best = cse3(n_in, rows, 0);
+    long bc = best.lop3();
+    for (int r = 1; r < g_cse_restarts; r++) {
+      Slp t = cse3(n_in, rows, (uint32_t)r);
+      const long c = t.lop3();
+      if (c < bc) { bc = c; best = std::move(t); }
+    }
+    return best;
+  }
   Slp s;
   s.n_in = n_in;
   s.rows = rows;
@@ -432,6 +443,7 @@ bool is_plain(const InputDesc &in) { return in.terms.size() == 1 && in.terms[0].
 
 std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st) {
   st = GenStats();
+  g_cse_restarts = std::max(1, o.cse_restarts);
   const int R = (int)p.outputs.size();
   const int C = (int)p.inputs.size();
   // ---- groups: output rows with identical support, split into chunks of max_rows ----
@@ -464,6 +476,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     std::vector<char> left(R, 1);
     int nleft = R;
     groups.clear();
+    st.clustered = true;
     while (nleft > 0) {
       int seed = -1;
       for (int r = 0; r < R; r++)

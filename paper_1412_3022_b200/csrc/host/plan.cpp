@@ -59,6 +59,21 @@ static std::string source_key(const std::string &src) {
 
 static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
   GenOptions oo = o;
+  {
+    // wide plans whose rows have distinct supports (decode: rows of G~^-1 over all B inputs, more
+    // than 8 outputs, >= 3 stages): groups of 16 rows on teams of 4 warps (2 rows each) halve the
+    // input transposes per output (measured: config-4 decode 1.14 -> 1.30 TB/s, profiles/r01d)
+    GenOptions p0 = oo;
+    if (p0.layout < 0) p0.layout = 0;
+    GenStats w0;
+    (void)generate_source(p, p0, w0);
+    if (o.auto_wide && w0.clustered && w0.max_stages >= 3 && p.outputs.size() > 8 && oo.team == 2 &&
+        oo.max_rows == 8) {
+      oo.max_rows = 16;
+      oo.team = 4;
+      if (oo.warps <= 0) oo.warps = 16;
+    }
+  }
   if (oo.layout < 0) {
     // group-specialised CTAs when the groups tile the 148 SMs with <= 10% left idle
     GenStats g0;
@@ -75,7 +90,7 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
   int w = std::max(1, std::min(16, budget / std::max(1, probe.smem_per_warp)));
   // measured (profiles/r01b): 12 warps for single-stage groups (encode); 8 for wide multi-stage
   // groups (decode: 4 stages of 14 inputs), where fewer, larger-register warps schedule better
-  int want = o.warps;
+  int want = oo.warps;
   if (want <= 0) want = probe.max_stages >= 3 ? 8 : 12;
   w = std::min(w, want);
   w = std::max(oo.team, w - w % std::max(1, oo.team));  // whole teams

@@ -50,6 +50,8 @@ struct GenOptions {
   int layout = -1;          // 0: every CTA walks all groups; 1: group-specialised CTAs; 2: same, CTAs
                             // apportioned by group cost; -1: auto
   int grid_ctas = 148;      // layout 2: CTAs the apportionment table is made for (one per SM)
+  bool auto_wide = true;    // resolve_options: 16-row groups on 4-warp teams for wide multi-stage plans
+  int cse_restarts = 1;     // CSE runs per network (seeded near-tie randomisation), keep the cheapest
   bool sched = false;       // register-pressure-aware temp order (emit_slp_sched) instead of CSE order
   int tr_unroll = 1;        // unroll factor of the in-place input transpose loop
   bool fence = true;        // register fence after every (sub-)network (see codegen.cpp)
@@ -67,6 +69,7 @@ struct GenStats {
   long loads = 0;        // 16-B vector loads per lane per item sum
   int smem_per_warp = 0; // bytes of shared memory (transposed input planes) per warp
   int max_stages = 0;    // most shared-memory stages of any group
+  bool clustered = false;  // rows had distinct supports and were clustered greedily
   double group_cost_ratio = 1;  // max / min estimated group cost (loaded blocks + outputs)
 };
 

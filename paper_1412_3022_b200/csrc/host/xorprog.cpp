@@ -103,7 +103,13 @@ Slp paar(int n_in, const std::vector<std::vector<int>> &rows_in) {
   return s;
 }
 
-Slp cse3(int n_in, const std::vector<std::vector<int>> &rows_in) {
+Slp cse3(int n_in, const std::vector<std::vector<int>> &rows_in, uint32_t seed) {
+  uint64_t rng = 0x9E3779B97F4A7C15ull * (seed + 1);
+  auto noise = [&]() -> double {  // [0, 0.5): breaks ties / explores near-best choices (seed != 0)
+    if (!seed) return 0.0;
+    rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+    return (double)(rng >> 40) / (double)(1ull << 24) * 0.5;
+  };
   Slp s;
   s.n_in = n_in;
   s.rows = rows_in;
@@ -151,7 +157,7 @@ Slp cse3(int n_in, const std::vector<std::vector<int>> &rows_in) {
     const int nsig = (int)sig_rows.size();
     for (auto &x : cand) {
       int c = std::get<0>(x), a = std::get<1>(x), b = std::get<2>(x);
-      if (c >= 3 && c * 0.5 - 1 > best) { best = c * 0.5 - 1; bops = {a, b}; }
+      if (c >= 3 && c * 0.5 - 1 + noise() > best) { best = c * 0.5 - 1; bops = {a, b}; }
       // best third signal among the rows containing a and b
       freq.assign(nsig, 0);
       int bc = -1, bcnt = 0;
@@ -166,7 +172,7 @@ Slp cse3(int n_in, const std::vector<std::vector<int>> &rows_in) {
           }
         }
       }
-      if (bcnt >= 2 && bcnt - 1.0 > best) {
+      if (bcnt >= 2 && bcnt - 1.0 + noise() > best) {
         best = bcnt - 1.0;
         bops = {a, b, bc};
       }

@@ -28,7 +28,8 @@ Slp paar(int n_in, const std::vector<std::vector<int>> &rows_in);
 // LOP3-aware CSE: greedily materialise the signal pair (used by >= 3 rows, saves ~r/2 - 1 LOP3) or
 // triple (used by >= 2 rows, saves r - 1) with the best saving; triples are found by extending the
 // top pairs with the best third signal among the rows that contain them.
-Slp cse3(int n_in, const std::vector<std::vector<int>> &rows_in);
+// seed != 0 randomises near-ties (restarts: keep the cheapest of several seeds).
+Slp cse3(int n_in, const std::vector<std::vector<int>> &rows_in, uint32_t seed = 0);
 
 // naive 3-input-LOP3 count of a bit matrix row set: sum ceil((ones-1)/2)
 long naive_lop3(const std::vector<std::vector<int>> &rows);

@@ -267,3 +267,109 @@ def test_full_size_config2_sampled():
         assert not par[stripes - 1, :, :].any() if full_blocks == 0 else True
     finally:
         pm.pmrc_destroy(code)
+
+
+def _full_job(kind, k, S, seed):
+    n, d = 2 * k, 2 * k - 2
+    code = pm.pmrc_create(kind, k, d, n)
+    info = pm.pmrc_info(code)
+    B, P, a = info["B"], info["parity_rows"], info["alpha"]
+    real = 1 << 30
+    stripes = -(-real // (B * S))
+    data = torch.empty((stripes, B, S), dtype=torch.uint8, device=DEV)
+    par = torch.empty((stripes, P, S), dtype=torch.uint8, device=DEV)
+    stream = torch.cuda.current_stream().cuda_stream
+    inputs.fill_device(data.data_ptr(), data.numel(), seed, real_len=real, stream=stream)
+    pm.pmrc_encode(code, data.data_ptr(), par.data_ptr(), S, stripes, stream)
+    torch.cuda.synchronize()
+    return code, data, par, (n, d, B, P, a, stripes, real, stream)
+
+
+def test_full_size_config4_repair_and_decode():
+    # config 4 at full size (1 GiB, 1 MiB sub-blocks, 19 stripes) in the sweep's launch
+    # configuration: a repair of a parity node (alpha blocks per helper) and of a systematic node
+    # (1 block per helper) regenerate the encoded pieces exactly; decode from a random
+    # 8-subset returns the data; a sampled window of the parity is checked against the oracle
+    k, S = 8, 1 << 20
+    code, data, par, (n, d, B, P, a, stripes, real, stream) = _full_job(pm.PMRC_MSR_SPARSE, k, S, 99)
+    try:
+        def piece(i):
+            return (par.data_ptr() + (i - k) * a * S, P * S) if i >= k else (data.data_ptr() + i * a * S, B * S)
+
+        def piece_t(i):
+            return par[:, (i - k) * a:(i - k + 1) * a] if i >= k else data[:, i * a:(i + 1) * a]
+        x = np.stack([inputs.host_bytes(2048, 99, 5 * B * S + c * S + 4096, real) for c in range(B)])
+        assert np.array_equal(par[5, :, 4096:4096 + 2048].cpu().numpy(), O.encode(O.MSR_SPARSE, n, k, d, x[None])[0])
+        out = torch.empty((stripes, a, S), dtype=torch.uint8, device=DEV)
+        for f, H in ((13, [i for i in range(n) if i not in (13, 9)]), (3, [i for i in range(n) if i not in (3, 11)])):
+            out.fill_(0)
+            pm.pmrc_repair(code, f, H, [piece(i) for i in H], (out.data_ptr(), a * S), S, stripes, stream)
+            torch.cuda.synchronize()
+            assert torch.equal(out, piece_t(f)), f
+        ids = sorted(inputs.rng(4).choice(n, k, replace=False).tolist())
+        dec = torch.zeros_like(data)
+        nw = pm.pmrc_decode(code, ids, [piece(i) for i in ids], dec.data_ptr(), S, stripes, stream)
+        torch.cuda.synchronize()
+        miss = [i * a + x for i in range(k) if i not in ids for x in range(a)]
+        assert nw == len(miss)
+        assert torch.equal(dec[:, miss], data[:, miss])
+    finally:
+        pm.pmrc_destroy(code)
+
+
+def test_full_size_config3_mbr_encode_decode():
+    # config 3 at full size (MBR k=8, 1 GiB, 256 KiB sub-blocks, 49 stripes): sampled parity windows
+    # vs the oracle, then decode from a random 8-subset of nodes returns every missing data block
+    k, S = 8, 256 << 10
+    code, data, par, (n, d, B, P, a, stripes, real, stream) = _full_job(pm.PMRC_MBR, k, S, 7)
+    try:
+        for t, p0 in ((0, 0), (stripes - 2, S - 1024), (17, 77 * 16)):
+            x = np.stack([inputs.host_bytes(1024, 7, t * B * S + c * S + p0, real) for c in range(B)])
+            assert np.array_equal(par[t, :, p0:p0 + 1024].cpu().numpy(), O.encode(O.MBR, n, k, d, x[None])[0])
+        L = pm.pmrc_layout(code)
+        ids = sorted(inputs.rng(3).choice(n, k, replace=False).tolist())
+        sysp = {}
+        pieces = []
+        for i in ids:
+            if i >= k:
+                pieces.append((par.data_ptr() + (i - k) * a * S, P * S))
+            else:                      # MBR systematic node i = row i of M(X) (R6), materialised
+                sysp[i] = data.index_select(1, torch.tensor([int(v) - 1 for v in L[i]], device=DEV)).contiguous()
+                pieces.append((sysp[i].data_ptr(), a * S))
+        dec = torch.zeros_like(data)
+        pm.pmrc_decode(code, ids, pieces, dec.data_ptr(), S, stripes, stream)
+        torch.cuda.synchronize()
+        held = set()
+        for i in ids:
+            if i < k:
+                held |= {int(v) - 1 for v in L[i]}
+        miss = sorted(set(range(B)) - held)
+        assert miss and torch.equal(dec[:, miss], data[:, miss])
+    finally:
+        pm.pmrc_destroy(code)
+
+
+def test_per_stripe_patterns_one_launch_each():
+    # config 4's per-stripe failure patterns: each stripe repaired / decoded with its own plan by
+    # offsetting the piece pointers to that stripe (stripes = 1 per launch)
+    k, n, S, stripes = 8, 16, 4096 + 512, 4
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=61)
+    try:
+        st.encode()
+        r = inputs.rng(12)
+        out = torch.zeros((stripes, st.alpha, S), dtype=torch.uint8, device=DEV)
+        want = []
+        for t in range(stripes):
+            while True:
+                f = int(r.integers(n))
+                H = sorted(r.choice([i for i in range(n) if i != f], st.d, replace=False).tolist())
+                if not _predicted_singular(pm.PMRC_MSR_SPARSE, k, n, f, H):
+                    break
+            pieces = [(st.piece(i)[0] + t * st.piece(i)[1], st.piece(i)[1]) for i in H]
+            pm.pmrc_repair(st.code, f, H, pieces, (out[t].data_ptr(), st.alpha * S), S, 1, st.stream)
+            want.append(st.piece_tensor(f)[t])
+        torch.cuda.synchronize()
+        for t in range(stripes):
+            assert torch.equal(out[t], want[t]), t
+    finally:
+        st.close()

@@ -113,6 +113,17 @@ static __device__ __forceinline__ bool pm_pace(const u64 *p, u32 stride, u32 n, 
   }
   return false;
 }
+// n / d by multiply-high (Granlund-Montgomery): magic from pm_udiv_setup(d) once per thread
+static __device__ __forceinline__ void pm_udiv_setup(u32 d, u32 &m, u32 &s1, u32 &s2) {
+  const u32 l = d > 1u ? 32u - __clz(d - 1u) : 0u;
+  m = (u32)(((1ull << 32) * ((1ull << l) - d)) / d) + 1u;
+  s1 = l < 1u ? l : 1u;
+  s2 = l > 0u ? l - 1u : 0u;
+}
+static __device__ __forceinline__ u32 pm_udiv(u32 n, u32 m, u32 s1, u32 s2) {
+  const u32 t = __umulhi(m, n);
+  return (t + ((n - t) >> s1)) >> s2;
+}
 static __device__ __forceinline__ u64 pm_gtime() {
   u64 t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -621,7 +632,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     const Stage &sg = stages[sid];
     const int n = (int)sg.blocks.size();
     o2 << ind << "{ const u32 gq = " << gi << ";\n";
-    o2 << ind << "  const u64 tt = gq / chunks;\n";
+    o2 << ind << "  const u64 tt = pm_udiv(gq, dv_m, dv_s1, dv_s2);\n";
     o2 << ind << "  const u64 qo = (u64)(gq - (u32)tt * chunks) * 1024u + lane * 16u;\n";
     o2 << ind << "  const bool okq = " << valid << ";\n";
     o2 << ind << "  const u32 z0 = (okq && qo < S) ? 16u : 0u, z1 = (okq && qo + 512u < S) ? 16u : 0u;\n";
@@ -703,6 +714,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
        "const u64 S, const u32 stripes, const u32 chunks, u64 *__restrict__ pace, const u32 epoch) {\n";
   s << "  extern __shared__ __align__(1024) unsigned char pm_smem[];\n";
   s << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, team = warp / PM_T, rank = warp - team * PM_T;\n";
+  s << "  u32 dv_m, dv_s1, dv_s2;\n  pm_udiv_setup(chunks, dv_m, dv_s1, dv_s2);\n";
   int first_sid = -1;
   for (size_t g = 0; g < groups.size() && first_sid < 0; g++)
     if (!gstages[g].empty()) first_sid = gstages[g][0];
@@ -906,7 +918,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     s << "    #pragma unroll 1\n";
     s << "    for (u32 m = 0; m < cnt; m++) {\n";
     s << "      const u32 gi = tb + m;\n";
-    s << "      const u64 t = gi / chunks;\n";
+    s << "      const u64 t = pm_udiv(gi, dv_m, dv_s1, dv_s2);\n";
     s << "      const u32 q = gi - (u32)t * chunks;\n";
     s << "      const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
     s << "      const bool v0 = o0 < S, v1 = o1 < S;\n";
@@ -982,7 +994,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         s << "      }\n";
       }
     }
-    s << "      const u64 t = gi / chunks;\n";
+    s << "      const u64 t = pm_udiv(gi, dv_m, dv_s1, dv_s2);\n";
     s << "      const u32 q = gi - (u32)t * chunks;\n";
     s << "      const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
     s << "      const bool v0 = o0 < S, v1 = o1 < S;\n";

@@ -262,6 +262,18 @@ def main():
         run_decode(j, rng, args.steps, "config4")
         run_config4_per_stripe(j, rng, args.steps)
         j.close()
+    if "next1" in cfgs:
+        # the paper's comparisons on the same kernel:
+        # vanilla vs sparse systematic MSR vs RS encode at k=4, 8 (1 GiB, 1 MiB sub-blocks), and
+        # MBR k=8 repair (a systematic and a parity node)
+        for k in (4, 8):
+            for kind in (MSR, VAN):
+                run_encode(kind, k, 2 * k, 1 << 20, args.steps).close()
+        run_encode(RS, 8, 16, 1 << 20, args.steps).close()
+        j = run_encode(MBR, 8, 16, 256 << 10, args.steps)
+        for _ in range(2):
+            run_repair(j, rng, args.steps, "next1-mbr")
+        j.close()
     if "5" in cfgs:
         for kind in (MSR, MBR):
             for k in [int(x) for x in args.ks.split(",")]:

@@ -24,11 +24,12 @@ int fail(int rc, const std::string &msg) {
   return rc;
 }
 
+constexpr int kHostBufs = 3;  // staging ring: H2D of chunk i+1/i+2 overlaps compute and D2H of chunk i
 struct HostStage {
   size_t chunk_stripes = 0;
-  void *d_data[2] = {nullptr, nullptr};
-  void *d_par[2] = {nullptr, nullptr};
-  cudaStream_t st[2] = {nullptr, nullptr};
+  void *d_data[kHostBufs] = {};
+  void *d_par[kHostBufs] = {};
+  cudaStream_t st[kHostBufs] = {};
   cudaEvent_t ev_start = nullptr;
   size_t bytes = 0;
 };
@@ -264,7 +265,7 @@ void pmrc_destroy(pmrc_code *c) {
   if (c->device >= 0 && have) cudaSetDevice(c->device);
   free_kernel(c->enc);
   for (auto &kv : c->plans) free_kernel(*kv.second);
-  for (int i = 0; i < 2; i++) {
+  for (int i = 0; i < kHostBufs; i++) {
     if (c->hs.d_data[i]) cudaFree(c->hs.d_data[i]);
     if (c->hs.d_par[i]) cudaFree(c->hs.d_par[i]);
     if (c->hs.st[i]) cudaStreamDestroy(c->hs.st[i]);
@@ -438,11 +439,11 @@ int pmrc_encode_host(pmrc_code *c, const void *data_host, void *parity_host, siz
   const CodeDef &D = c->def;
   HostStage &h = c->hs;
   const size_t in_b = (size_t)D.B * S, out_b = (size_t)D.P * S;
-  // chunks of ~64 MiB of source data, double buffered
+  // chunks of ~64 MiB of source data, a ring of kHostBufs buffers / streams
   size_t chunk = std::max<size_t>(1, ((size_t)64 << 20) / in_b);
   chunk = std::min(chunk, stripes);
   if (h.chunk_stripes < chunk) {
-    for (int i = 0; i < 2; i++) {
+    for (int i = 0; i < kHostBufs; i++) {
       if (h.d_data[i]) cudaFree(h.d_data[i]);
       if (h.d_par[i]) cudaFree(h.d_par[i]);
       h.d_data[i] = h.d_par[i] = nullptr;
@@ -454,18 +455,18 @@ int pmrc_encode_host(pmrc_code *c, const void *data_host, void *parity_host, siz
     }
     h.chunk_stripes = chunk;
   }
-  for (int i = 0; i < 2; i++)
+  for (int i = 0; i < kHostBufs; i++)
     if (!h.st[i] && cudaStreamCreateWithFlags(&h.st[i], cudaStreamNonBlocking) != cudaSuccess)
       return fail(PMRC_ECUDA, "stream create");
   if (!h.ev_start && cudaEventCreateWithFlags(&h.ev_start, cudaEventDisableTiming) != cudaSuccess)
     return fail(PMRC_ECUDA, "event create");
   // order after the caller's stream
   cudaEventRecord(h.ev_start, (cudaStream_t)stream);
-  for (int i = 0; i < 2; i++) cudaStreamWaitEvent(h.st[i], h.ev_start, 0);
+  for (int i = 0; i < kHostBufs; i++) cudaStreamWaitEvent(h.st[i], h.ev_start, 0);
   size_t idx = 0;
   for (size_t s0 = 0; s0 < stripes; s0 += chunk, idx++) {
     const size_t ns = std::min(chunk, stripes - s0);
-    const int b = (int)(idx & 1);
+    const int b = (int)(idx % kHostBufs);
     cudaStream_t st = h.st[b];
     if (cudaMemcpyAsync(h.d_data[b], (const uint8_t *)data_host + s0 * in_b, ns * in_b, cudaMemcpyHostToDevice, st) !=
         cudaSuccess)
@@ -479,7 +480,7 @@ int pmrc_encode_host(pmrc_code *c, const void *data_host, void *parity_host, siz
         cudaSuccess)
       return fail(PMRC_ECUDA, "D2H copy");
   }
-  for (int i = 0; i < 2; i++)
+  for (int i = 0; i < kHostBufs; i++)
     if (cudaStreamSynchronize(h.st[i]) != cudaSuccess) return fail(PMRC_ECUDA, cudaGetErrorString(cudaGetLastError()));
   return PMRC_OK;
 }

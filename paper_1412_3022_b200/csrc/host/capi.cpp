@@ -192,7 +192,7 @@ const char *pmrc_strerror(int err) {
 
 const char *pmrc_last_error(void) { return g_last_error.c_str(); }
 
-unsigned long long pmrc_launch_count(void) { return launch_counter(); }
+unsigned long long pmrc_launch_count(void) { return launch_counter().load(); }
 
 int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
   if (!out) return fail(PMRC_EINVAL, "out is NULL");

@@ -418,13 +418,11 @@ void emit_slp(std::ostringstream &s, const Slp &p, const std::vector<std::string
   emit_slp_lazy(s, p, base, outs, accumulate, tpref, [](const std::string &) {});
 }
 
-int g_cse_restarts = 1;  // set from GenOptions by generate_source
-
-Slp make_slp(int n_in, const std::vector<std::vector<int>> &rows, bool cse) {
+Slp make_slp(int n_in, const std::vector<std::vector<int>> &rows, bool cse, int restarts = 1) {
   if (cse) {
     Slp best = cse3(n_in, rows, 0);
     long bc = best.lop3();
-    for (int r = 1; r < g_cse_restarts; r++) {
+    for (int r = 1; r < restarts; r++) {
       Slp t = cse3(n_in, rows, (uint32_t)r);
       const long c = t.lop3();
       if (c < bc) { bc = c; best = std::move(t); }
@@ -454,7 +452,6 @@ bool is_plain(const InputDesc &in) { return in.terms.size() == 1 && in.terms[0].
 
 std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st) {
   st = GenStats();
-  g_cse_restarts = std::max(1, o.cse_restarts);
   const int R = (int)p.outputs.size();
   const int C = (int)p.inputs.size();
   // ---- groups: output rows with identical support, split into chunks of max_rows ----
@@ -777,7 +774,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
                   if ((br[bb] >> bp) & 1) drows[bb].push_back((int)u * 8 + bp);
               }
             }
-            Slp ds = make_slp((int)dbase.size(), drows, o.cse);
+            Slp ds = make_slp((int)dbase.size(), drows, o.cse, o.cse_restarts);
             if (rk == 0) {
               st.xor2 += ds.xor2();
               st.naive_lop3 += naive_lop3(drows);
@@ -815,7 +812,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
             for (size_t r = 0; r < rows.size(); r++)
               for (int x : rows[r])
                 if (x >= 8 * c0 && x < 8 * c1) sr[r].push_back(x - 8 * c0);
-            subs.push_back(make_slp(8 * (c1 - c0), sr, o.cse));
+            subs.push_back(make_slp(8 * (c1 - c0), sr, o.cse, o.cse_restarts));
             sub_base.emplace_back(base.begin() + 8 * c0, base.begin() + 8 * c1);
             const bool acc = !(first && c0 == 0);
             st.xor2 += subs.back().xor2() + (acc ? 8 * m : 0);

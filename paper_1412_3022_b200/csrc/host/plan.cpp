@@ -9,6 +9,7 @@
 #include <sys/stat.h>
 
 #include <algorithm>
+#include <atomic>
 #include <fstream>
 #include <chrono>
 #include <unistd.h>
@@ -22,8 +23,8 @@
 
 namespace pmrc {
 
-unsigned long long &launch_counter() {
-  static unsigned long long c = 0;
+std::atomic<unsigned long long> &launch_counter() {
+  static std::atomic<unsigned long long> c{0};
   return c;
 }
 

@@ -8,6 +8,7 @@
 // region-linear-combination kernel").  An input may itself be a small combination of blocks
 // ("derived" input, used by the fused repair: beta_h = phi_f . piece_h).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -112,6 +113,6 @@ int precompile_kernel(const PlanSpec &p, const GenOptions &o, std::string &err);
 int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides, size_t S, size_t stripes,
                   void *stream, std::string &err);
 
-unsigned long long &launch_counter();
+std::atomic<unsigned long long> &launch_counter();
 
 }  // namespace pmrc

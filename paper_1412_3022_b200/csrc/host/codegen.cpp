@@ -83,6 +83,7 @@ static __device__ __forceinline__ u64 pm_policy_en() {
 }
 static __device__ __forceinline__ void pm_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 static __device__ __forceinline__ void pm_cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N> static __device__ __forceinline__ void pm_cp_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 static __device__ __forceinline__ void pm_team_sync(u32 id, u32 n) { asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory"); }
 static __device__ __forceinline__ void pm_bar_init(u32 bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar) : "memory");
@@ -568,6 +569,9 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   }
 
   const int M = std::max(1, o.chunk_loop);
+  // stage-buffer ring per team: NB buffers, prefetch distance D = NB - 1 stages (layouts 1/2)
+  const int NB = o.layout == 0 ? 2 : std::max(2, o.nbuf);
+  const int D = NB - 1;
   const int T = std::max(1, o.team);  // warps sharing one chunk's stage buffer
   std::ostringstream s;
   s << "// generated by libpmrc (codegen.cpp) — bitsliced GF(2^8) region linear combination\n";
@@ -742,7 +746,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         const int nblk = (int)sg.blocks.size();
         s << "        {\n";
         // consume: own copies landed -> transpose own share -> team barrier
-        s << "          pm_cp_wait0();\n";
+        s << "          pm_cp_wait<" << (D - 1) << ">();\n";
         s << "          const u32 buf = sbuf + pb * (PM_QMAX * 1024u);\n";
         s << "          pm_transpose_in(buf + lane * 16u, " << nblk * rk / T << "u, " << nblk * (rk + 1) / T << "u);\n";
         s << "          " << (T > 1 ? "pm_team_sync(1u + team, PM_T * 32u);" : "__syncwarp();") << "\n";
@@ -856,7 +860,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
           s << net.str();
           first = false;
         }
-        s << "          pb ^= 1u;\n";
+        s << (NB == 2 ? "          pb ^= 1u;\n" : "          pb = pb + 1u == " + std::to_string(NB) + "u ? 0u : pb + 1u;\n");
         s << "        }\n";
         if (rk == 0) {
           st.loads += nblk;
@@ -890,7 +894,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   s << "  const u32 total = stripes * chunks;\n";
   s << "  const u32 per_cta = (total + gridDim.x - 1u) / gridDim.x;\n";
   s << "  const u32 c0 = blockIdx.x * per_cta, c1 = min(total, c0 + per_cta);\n";
-  s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (2u * PM_QMAX * 1024u);\n";
+  s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (" << NB << "u * PM_QMAX * 1024u);\n";
   s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en();\n";
   s << "  u32 pb = 0u;\n";
   if (first_sid >= 0) {
@@ -954,7 +958,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   }
   s << "  const u32 total = stripes * chunks;\n";
   s << "  const u32 c0 = (u32)((u64)total * r / spg), c1 = (u32)((u64)total * (r + 1u) / spg);\n";
-  s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (2u * PM_QMAX * 1024u);\n";
+  s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (" << NB << "u * PM_QMAX * 1024u);\n";
   s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en();\n";
   s << "  u32 pb = 0u;\n";
   s << "  bool pacing = pace != 0;\n";
@@ -962,12 +966,19 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   s << "  switch (g) {\n";
   for (size_t g = 0; g < groups.size(); g++) {
     s << "  case " << g << ": {\n";
-    if (!gstages[g].empty()) {
-      s << "    if (c0 + team < c1) {\n";
-      emit_issue(s, gstages[g][0], "c0 + team", "true", "0u", "      ");
-      s << "    }\n";
+    {
+      const int ns = (int)gstages[g].size();
+      for (int pp = 0; pp < D; pp++) {
+        if (ns) {
+          const int di = pp / ns, sid = gstages[g][pp % ns];
+          const std::string it = "c0 + team + " + std::to_string(di) + "u * teams";
+          s << "    if (" << it << " < c1) {\n";
+          emit_issue(s, sid, it, "true", std::to_string(pp % NB) + "u", "      ");
+          s << "    }\n";
+        }
+        s << "    pm_cp_commit();\n";
+      }
     }
-    s << "    pm_cp_commit();\n";
     s << "    #pragma unroll 1\n";
     s << "    for (u32 gi = c0 + team, kk = 0; gi < c1; gi += teams, kk++) {\n";
     const bool pace_async = o.pace_lag > 0 && groups.size() <= 32;
@@ -996,12 +1007,17 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     s << "      const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
     s << "      const bool v0 = o0 < S, v1 = o1 < S;\n";
     emit_body(g, [&](size_t gg, size_t sj) {
-      if (sj + 1 < gstages[gg].size()) {
-        emit_issue(s, gstages[gg][sj + 1], "gi", "true", "pb ^ 1u", "          ");
+      const int ns = (int)gstages[gg].size();
+      const int di = ((int)sj + D) / ns, sid = gstages[gg][((int)sj + D) % ns];
+      const std::string bb = NB == 2 ? std::string("pb ^ 1u")
+                                     : "(pb + " + std::to_string(D) + "u) % " + std::to_string(NB) + "u";
+      if (di == 0) {
+        emit_issue(s, sid, "gi", "true", bb, "          ");
         return;
       }
-      s << "          if (gi + teams < c1) {\n";
-      emit_issue(s, gstages[gg][0], "gi + teams", "true", "pb ^ 1u", "            ");
+      const std::string it = "gi + " + std::to_string(di) + "u * teams";
+      s << "          if (" << it << " < c1) {\n";
+      emit_issue(s, sid, it, "true", bb, "            ");
       s << "          }\n";
     });
     if (o.pace_lag > 0)
@@ -1028,7 +1044,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   }
   s << "}\n";
   }
-  st.smem_per_warp = (2 * qmax * 1024 + T - 1) / T;
+  st.smem_per_warp = (NB * qmax * 1024 + T - 1) / T;
   for (auto &gs : gstages) st.max_stages = std::max(st.max_stages, (int)gs.size());
   return s.str();
 }

@@ -171,7 +171,7 @@ int pmrc_plan_stats(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids
 
 /* Diagnostics of the encode kernel's CTA pacing (group-specialised layout): copies the device
  * counter area (5 x E u64: progress counters, then per-(CTA, team) start / end globaltimer ns, ns
- * spent pacing and pacing timeouts, the last four only with PMRC_GEN=trace=1) to host[0..cap) and
+ * spent pacing and (group << 32 | pacing timeouts), the last four only with PMRC_GEN=trace=1) to host[0..cap) and
  * its length to *n (0 if the encode kernel has no counters).  Synchronous (cudaMemcpy); not part
  * of the data path. */
 int pmrc_debug_counters(const pmrc_code *c, unsigned long long *host, size_t cap, size_t *n);

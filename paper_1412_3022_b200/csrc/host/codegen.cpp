@@ -662,10 +662,11 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   };
 
   if (o.layout == 2) {
-    // layout 2: groups of unequal cost (MBR: d- and k-input groups) get CTAs in proportion to
-    // their estimated instruction count, from a table for a grid of PM_NG CTAs (plan.cpp)
-    std::vector<double> w(groups.size());
-    double tot = 0;
+    // layout 2: groups of unequal cost (MBR: d- and k-input groups).  The (group, chunk) work is
+    // laid out group-major with an estimated cost per chunk of each group, and every CTA takes an
+    // equal-cost slice: at most two groups per CTA, run one after the other (so each SM still
+    // executes one group's code at a time), and all CTAs finish together.
+    std::vector<long> cw(groups.size() + 1, 0);
     for (size_t g = 0; g < groups.size(); g++) {
       long ones = 0;
       for (int r : groups[g].rows)
@@ -677,37 +678,13 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
           }
       long nblk = 0;
       for (int c : groups[g].cols) nblk += (long)p.inputs[c].terms.size();
-      w[g] = 48.0 * (double)(nblk + (long)groups[g].rows.size()) + 0.3 * (double)ones + 150.0;
-      tot += w[g];
+      // per-chunk cost: transposes (48 instructions per block), XOR work, fixed per-item overhead
+      const long w = 48 * (nblk + (long)groups[g].rows.size()) + (3 * ones) / 10 + 300;
+      cw[g + 1] = cw[g] + w;
     }
-    const int NG = std::max<int>((int)groups.size(), o.grid_ctas);
-    std::vector<int> n(groups.size(), 1);
-    int used = (int)groups.size();
-    // largest-remainder apportionment of the remaining CTAs
-    std::vector<double> want(groups.size());
-    for (size_t g = 0; g < groups.size(); g++) want[g] = NG * w[g] / tot;
-    while (used < NG) {
-      size_t bg = 0;
-      double bd = -1e30;
-      for (size_t g = 0; g < groups.size(); g++) {
-        const double d = want[g] - n[g];
-        if (d > bd) { bd = d; bg = g; }
-      }
-      n[bg]++;
-      used++;
-    }
-    s << "#define PM_NG " << NG << "u\n";
-    std::ostringstream tg, tr, tn;
-    int k = 0;
-    for (size_t g = 0; g < groups.size(); g++)
-      for (int r = 0; r < n[g]; r++, k++) {
-        tg << (k ? ", " : "") << g;
-        tr << (k ? ", " : "") << r;
-        tn << (k ? ", " : "") << n[g];
-      }
-    s << "__constant__ unsigned short pm_cta_g[" << NG << "] = {" << tg.str() << "};\n";
-    s << "__constant__ unsigned short pm_cta_r[" << NG << "] = {" << tr.str() << "};\n";
-    s << "__constant__ unsigned short pm_cta_n[" << NG << "] = {" << tn.str() << "};\n";
+    s << "__constant__ unsigned int pm_cw[" << cw.size() << "] = {";
+    for (size_t g = 0; g < cw.size(); g++) s << (g ? ", " : "") << cw[g] << "u";
+    s << "};\n";
   }
   const int TPB = 32 * std::max(T, o.warps);
   const int teams = TPB / 32 / T;
@@ -950,19 +927,29 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   // second read hits L2) and each SM only ever executes one group's code (instruction cache).
   // Teams interleave over the range (team, team + teams, ...) so all groups advance in step.
   s << "  const u32 teams = " << teams << "u;\n";
-  if (o.layout == 2) {
-    s << "  if (blockIdx.x >= PM_NG) return;\n";
-    s << "  const u32 g = pm_cta_g[blockIdx.x], r = pm_cta_r[blockIdx.x], spg = pm_cta_n[blockIdx.x];\n";
-  } else {
-    s << "  const u32 spg = gridDim.x / " << groups.size() << "u, g = blockIdx.x / spg, r = blockIdx.x - g * spg;\n";
-  }
-  s << "  const u32 total = stripes * chunks;\n";
-  s << "  const u32 c0 = (u32)((u64)total * r / spg), c1 = (u32)((u64)total * (r + 1u) / spg);\n";
   s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (" << NB << "u * PM_QMAX * 1024u);\n";
   s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en();\n";
   s << "  u32 pb = 0u;\n";
   s << "  bool pacing = pace != 0;\n";
   if (o.trace) s << "  const u64 tr_t0 = pm_gtime(); u64 tr_wait = 0; u32 tr_fail = 0;\n";
+  if (o.layout == 2) {
+    const size_t G = groups.size();
+    s << "  const u32 r = 0u, spg = 1u;  // (pacing is layout-1 only)\n";
+    s << "  const u64 Ct = (u64)stripes * chunks, Wt = Ct * " << "pm_cw[" << G << "];\n";
+    s << "  const u64 x0 = Wt * blockIdx.x / gridDim.x, x1 = Wt * (blockIdx.x + 1u) / gridDim.x;\n";
+    s << "  u32 g = 0u;\n";
+    s << "  for (u32 gs = 0; gs < " << G << "u; gs++) {\n";
+    s << "  const u64 s0 = Ct * pm_cw[gs], s1 = Ct * pm_cw[gs + 1u];\n";
+    s << "  if (s1 <= x0 || s0 >= x1) continue;\n";
+    s << "  const u64 wg = pm_cw[gs + 1u] - pm_cw[gs];\n";
+    s << "  const u64 lo = (x0 > s0 ? x0 : s0) - s0, hi = (x1 < s1 ? x1 : s1) - s0;\n";
+    s << "  const u32 c0 = (u32)((lo + wg - 1u) / wg), c1 = (u32)((hi + wg - 1u) / wg);\n";
+    s << "  g = gs;\n  pb = 0u;\n";
+  } else {
+    s << "  const u32 spg = gridDim.x / " << groups.size() << "u, g = blockIdx.x / spg, r = blockIdx.x - g * spg;\n";
+    s << "  const u32 total = stripes * chunks;\n";
+    s << "  const u32 c0 = (u32)((u64)total * r / spg), c1 = (u32)((u64)total * (r + 1u) / spg);\n";
+  }
   s << "  switch (g) {\n";
   for (size_t g = 0; g < groups.size(); g++) {
     s << "  case " << g << ": {\n";
@@ -981,8 +968,9 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     }
     s << "    #pragma unroll 1\n";
     s << "    for (u32 gi = c0 + team, kk = 0; gi < c1; gi += teams, kk++) {\n";
-    const bool pace_async = o.pace_lag > 0 && groups.size() <= 32;
-    if (o.pace_lag > 0) {
+    const int pace_lag = o.layout == 1 ? o.pace_lag : 0;  // pacing assumes aligned (layout 1) ranges
+    const bool pace_async = pace_lag > 0 && groups.size() <= 32;
+    if (pace_lag > 0) {
       // stay within pace_lag chunks of the slowest CTA of the same range (all groups).  Only rank 0
       // paces (rank 1 meets it at the team barrier).  The peers' counters for the next iteration
       // are loaded here and tested after this iteration's work, so the L2 round trip (several us
@@ -994,10 +982,10 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         s << "      if (pacing && rank == 0u && lane < " << groups.size() << "u)\n";
         s << "        asm volatile(\"ld.relaxed.gpu.global.u64 %0, [%1];\" : \"=l\"(pv) : \"l\"(pace + (r + lane * spg) * teams + team));\n";
       } else {
-        s << "      if (pacing && rank == 0u && kk > " << o.pace_lag << "u) {\n";
+        s << "      if (pacing && rank == 0u && kk > " << pace_lag << "u) {\n";
         if (o.trace) s << "        const u64 tw = pm_gtime();\n";
         s << "        pacing = pm_pace(pace + r * teams + team, spg * teams, " << groups.size()
-          << "u, ((u64)epoch << 32) | (kk - " << o.pace_lag << "u), lane);\n";
+          << "u, ((u64)epoch << 32) | (kk - " << pace_lag << "u), lane);\n";
         if (o.trace) s << "        tr_wait += pm_gtime() - tw; tr_fail += pacing ? 0u : 1u;\n";
         s << "      }\n";
       }
@@ -1020,11 +1008,11 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
       emit_issue(s, sid, it, "true", bb, "            ");
       s << "          }\n";
     });
-    if (o.pace_lag > 0)
+    if (pace_lag > 0)
       s << "      if (pace && rank == 0u && lane == 0u) pm_pace_post(pace + blockIdx.x * teams + team, ((u64)epoch << 32) | (kk + 1u));\n";
     if (pace_async) {
-      s << "      if (pacing && rank == 0u && kk + 1u > " << o.pace_lag << "u) {\n";
-      s << "        const u64 want = ((u64)epoch << 32) | (kk + 1u - " << o.pace_lag << "u);\n";
+      s << "      if (pacing && rank == 0u && kk + 1u > " << pace_lag << "u) {\n";
+      s << "        const u64 want = ((u64)epoch << 32) | (kk + 1u - " << pace_lag << "u);\n";
       s << "        if (!__all_sync(0xffffffffu, pv >= want)) {\n";
       if (o.trace) s << "          const u64 tw = pm_gtime();\n";
       s << "          pacing = pm_pace(pace + r * teams + team, spg * teams, " << groups.size() << "u, want, lane);\n";
@@ -1035,11 +1023,13 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     s << "  } break;\n";
   }
   s << "  default: break;\n  }\n";
+  if (o.layout == 2) s << "  }\n";  // segment loop
   if (o.trace) {
-    // diagnostics (E = 4096 entries per field, plan.cpp): [E + i] start, [2E + i] end (globaltimer ns), [3E + i] ns spent pacing, [4E + i] timeouts
+    // diagnostics (E = 4096 entries per field, plan.cpp): [E + i] start, [2E + i] end (globaltimer ns),
+    // [3E + i] ns spent pacing, [4E + i] = group << 32 | pacing timeouts
     s << "  if (pace && rank == 0u && lane == 0u) {\n";
     s << "    const u32 E = 4096u, i = blockIdx.x * teams + team;\n";
-    s << "    pace[E + i] = tr_t0; pace[2u * E + i] = pm_gtime(); pace[3u * E + i] = tr_wait; pace[4u * E + i] = tr_fail;\n";
+    s << "    pace[E + i] = tr_t0; pace[2u * E + i] = pm_gtime(); pace[3u * E + i] = tr_wait; pace[4u * E + i] = ((u64)g << 32) | tr_fail;\n";
     s << "  }\n";
   }
   s << "}\n";

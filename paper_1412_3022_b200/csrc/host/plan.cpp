@@ -218,7 +218,7 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
   int sms = 148;
   D.DeviceGetAttribute(&sms, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev);
   k.sms = sms;
-  if (k.layout == 1 && (oo.pace_lag > 0 || oo.trace)) {
+  if ((k.layout == 1 && oo.pace_lag > 0) || (k.layout >= 1 && oo.trace)) {
     k.pace_entries = 4096;  // per field; 5 fields (progress, then trace: start, end, wait, timeouts)
     if (cudaMalloc(&k.pace, k.pace_entries * 8 * 6) != cudaSuccess ||
         cudaMemset(k.pace, 0, k.pace_entries * 8 * 6) != cudaSuccess) {
@@ -261,7 +261,7 @@ int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides
     // the kernel splits the ns * chunks chunk range evenly over the CTAs
     uint64_t grid = (uint64_t)k.sms * k.blocks_per_sm;
     if (k.layout == 2) {
-      grid = (uint64_t)std::max(k.n_groups, oo_grid(k));
+      grid = (uint64_t)oo_grid(k);  // equal-cost slices, one per CTA
     } else if (k.layout == 1) {
       // group-specialised: G groups x spg chunk ranges (grid must be a multiple of G)
       const uint64_t G = (uint64_t)k.n_groups;

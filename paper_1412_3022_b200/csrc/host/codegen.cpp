@@ -726,11 +726,15 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         s << "          pm_cp_wait<" << (D - 1) << ">();\n";
         s << "          const u32 buf = sbuf + pb * (PM_QMAX * 1024u);\n";
         s << "          pm_transpose_in(buf + lane * 16u, " << nblk * rk / T << "u, " << nblk * (rk + 1) / T << "u);\n";
-        s << "          " << (T > 1 ? "pm_team_sync(1u + team, PM_T * 32u);" : "__syncwarp();") << "\n";
-        // prefetch the successor stage into the other buffer
-        prefetch(g, sj);
-        s << "          pm_cp_commit();\n";
         s << "          const u32 pl = buf + lane * 16u;\n";
+        // the team barrier + the prefetch of the successor stage into the other buffer; emitted
+        // after the sub-networks that read only this warp's own transposed blocks (below)
+        auto emit_sync = [&]() {
+          s << "          " << (T > 1 ? "pm_team_sync(1u + team, PM_T * 32u);" : "__syncwarp();") << "\n";
+          prefetch(g, sj);
+          s << "          pm_cp_commit();\n";
+        };
+        if (m == 0) emit_sync();
         if (m > 0) {
           std::vector<std::string> base;
           std::vector<char> used_half(2 * nblk, 0);
@@ -800,20 +804,33 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
             st.xor2_naive += make_slp(8 * (c1 - c0), sr, false).xor2() + (acc ? 8 * m : 0);
           }
           st.naive_lop3 += naive_lop3(rows);
-          std::vector<char> loaded(2 * nblk, 0);
-          std::ostringstream net;
-          auto need = [&](const std::string &nmb) {
-            if (nmb[0] != 'P') return;
-            int h = std::stoi(nmb.substr(1, nmb.find('.') - 1));
-            if (loaded[h]) return;
-            loaded[h] = 1;
-            net << "          const uint4 P" << h << " = pm_lds(pl + " << (h / 2) * 1024 + (h % 2) * 512 << "u);\n";
-          };
-          for (int h = 0; h < 2 * nblk; h++)
-            if (used_half[h] && !loaded[h]) need("P" + std::to_string(h) + ".x");
-          net << body.str();
+          // sub-networks whose inputs are all plain blocks this warp transposed itself run before
+          // the team barrier (their planes are already in place), the rest after it
+          const int own_lo = nblk * rk / T, own_hi = nblk * (rk + 1) / T;
+          std::vector<int> order_pre, order_post;
           for (size_t si2 = 0; si2 < subs.size(); si2++) {
-            const bool acc = !(first && si2 == 0);
+            bool own = T > 1 && o.own_first;
+            const int cc0 = (int)si2 * sub, cc1 = std::min(ncols, cc0 + sub);
+            for (int ci = cc0; ci < cc1 && own; ci++) {
+              const InputDesc &in = p.inputs[sg.cols[ci]];
+              const int fb = sg.first_block[ci];
+              own = is_plain(in) && fb >= own_lo && fb < own_hi;
+            }
+            (own ? order_pre : order_post).push_back((int)si2);
+          }
+          std::vector<char> loaded(2 * nblk, 0);
+          int emitted = 0;
+          auto emit_sub = [&](int si2) {
+            std::ostringstream net;
+            auto need = [&](const std::string &nmb) {
+              if (nmb[0] != 'P') return;
+              int h = std::stoi(nmb.substr(1, nmb.find('.') - 1));
+              if (loaded[h]) return;
+              loaded[h] = 1;
+              net << "          const uint4 P" << h << " = pm_lds(pl + " << (h / 2) * 1024 + (h % 2) * 512 << "u);\n";
+            };
+            const bool acc = !(first && emitted == 0);
+            emitted++;
             const std::string tp = subs.size() > 1 ? "t" + std::to_string(si2) + "_" : "t";
             if (subs.size() > 1) net << "          {\n";
             if (o.fold && o.sched)
@@ -833,8 +850,21 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
                 net << ");\n";
               }
             }
+            s << net.str();
+          };
+          for (int si2 : order_pre) emit_sub(si2);
+          emit_sync();
+          {
+            // planes of derived inputs (fused repair projections) after the barrier
+            std::ostringstream pre;
+            for (int h = 0; h < 2 * nblk; h++)
+              if (used_half[h] && !loaded[h]) {
+                loaded[h] = 1;
+                pre << "          const uint4 P" << h << " = pm_lds(pl + " << (h / 2) * 1024 + (h % 2) * 512 << "u);\n";
+              }
+            s << pre.str() << body.str();
           }
-          s << net.str();
+          for (int si2 : order_post) emit_sub(si2);
           first = false;
         }
         s << (NB == 2 ? "          pb ^= 1u;\n" : "          pb = pb + 1u == " + std::to_string(NB) + "u ? 0u : pb + 1u;\n");

@@ -45,7 +45,11 @@ enum {
   PMRC_MSR_SPARSE = 0,       /* the paper's sparse MSR: Phi = [I; Cauchy], Lambda Moebius */
   PMRC_MSR_VANILLA = 1,      /* Rashmi et al. Vandermonde MSR */
   PMRC_MBR = 2,              /* systematic MBR, Psi = [I_k 0; Cauchy] (R5) */
-  PMRC_RS_VANDERMONDE = 3    /* systematic Vandermonde Reed-Solomon baseline (R12); d = k */
+  PMRC_RS_VANDERMONDE = 3,   /* systematic Vandermonde Reed-Solomon baseline (R12); d = k */
+  PMRC_MSR_SPARSE_N2K = 4    /* EXTENSION, not the paper's: the sparse Phi = [I; Cauchy] with Lambda
+                                chosen greedily (R15) so that every d-row subset of Psi is
+                                invertible at n = 2k too: repair never returns PMRC_ESINGULAR
+                                (SURVEY §8(c) A7, §8(f) NEXT-4); n <= 41 */
 };
 
 /* error codes */

@@ -14,6 +14,7 @@ import subprocess
 import numpy as np
 
 MSR_SPARSE, MSR_VANILLA, MBR, RS = 0, 1, 2, 3
+MSR_N2K = 4   # extension (R15): sparse Phi, greedy Lambda valid at n = 2k; not the paper's
 OK, EINVAL, EUNSUP, ESING = 0, -1, -2, -3
 
 _HERE = os.path.dirname(os.path.abspath(__file__))

@@ -36,7 +36,11 @@
 #define OR_EUNSUP -2
 #define OR_ESING -3
 
-enum { OR_MSR_SPARSE = 0, OR_MSR_VANILLA = 1, OR_MBR = 2, OR_RS = 3 };
+enum { OR_MSR_SPARSE = 0, OR_MSR_VANILLA = 1, OR_MBR = 2, OR_RS = 3, OR_MSR_N2K = 4 };
+/* kind 4 is an EXTENSION, not the paper's construction (R15): the sparse Phi with a
+ * Lambda chosen greedily so that the code is valid at n = 2k.  It is an MSR code in every other
+ * respect (parameters, L, linearisation, decode, repair). */
+#define OR_IS_MSR(kind) ((kind) == OR_MSR_SPARSE || (kind) == OR_MSR_VANILLA || (kind) == OR_MSR_N2K)
 
 /* ------------------------------------------------------------------ GF(2^8), R1 */
 static uint8_t EXPT[512];
@@ -142,7 +146,7 @@ int or_mat_rank(const uint8_t *A, int r, int c) {
 /* ------------------------------------------------------------------ parameters */
 int or_params(int kind, int n, int k, int d, int *alpha, int *B) {
   if (k < 1 || n < 1) return OR_EINVAL;
-  if (kind == OR_MSR_SPARSE || kind == OR_MSR_VANILLA) {
+  if (OR_IS_MSR(kind)) {
     /* MSR: alpha = Delta = d - k + 1; the PM construction needs d = 2k-2 (R7) */
     if (k < 2 || d != 2 * k - 2 || n <= d) return OR_EUNSUP;
     *alpha = d - k + 1;
@@ -171,7 +175,7 @@ int or_params(int kind, int n, int k, int d, int *alpha, int *B) {
  * Symmetric blocks are numbered row-major over their upper triangle (R4, reproduces P:77-83). */
 int or_index_matrix(int kind, int k, int d, int *L) {
   int alpha, B;
-  if (kind == OR_MSR_SPARSE || kind == OR_MSR_VANILLA) {
+  if (OR_IS_MSR(kind)) {
     int rc = or_params(kind, d + 1, k, d, &alpha, &B);
     if (rc) return rc;
     int v = 1;
@@ -247,6 +251,50 @@ int or_psi(int kind, int n, int k, int d, uint8_t *psi, uint8_t *lambda) {
         psi[(i - 1) * d + alpha + (j - 1)] = or_gf_mul(lam, phi);
       }
     }
+    return OR_OK;
+  }
+  if (kind == OR_MSR_N2K) {
+    /* R15 (extension): Phi as in the sparse code; for i = 1..n in order, Lambda_{i,i} =
+       g^e with the smallest e >= 0 such that it differs from Lambda_{1..i-1} and every d-row
+       subset of Psi's rows 1..i that contains row i has rank d. */
+    if (n + alpha > 254 || n > 41) return OR_EUNSUP;
+    uint8_t *lam = (uint8_t *)malloc(n), *M = (uint8_t *)malloc((size_t)d * d);
+    int *c = (int *)malloc(sizeof(int) * (d > 1 ? d : 1));
+    for (int i = 1; i <= n; i++) {
+      uint8_t xi = or_gf_exp(i + alpha);
+      int found = 0;
+      for (int e = 0; e < 255 && !found; e++) {
+        uint8_t l = or_gf_exp(e);
+        int clash = 0;
+        for (int j = 1; j < i; j++)
+          if (lam[j - 1] == l) clash = 1;
+        if (clash) continue;
+        for (int j = 1; j <= alpha; j++) {
+          uint8_t phi = (i <= alpha) ? (uint8_t)(i == j) : or_gf_inv(xi ^ or_gf_exp(j - 1));
+          psi[(i - 1) * d + (j - 1)] = phi;
+          psi[(i - 1) * d + alpha + (j - 1)] = or_gf_mul(l, phi);
+        }
+        int ok = 1;
+        if (i >= d) {
+          /* every choice of d-1 rows among rows 1..i-1, plus row i */
+          for (int q = 0; q < d - 1; q++) c[q] = q;
+          for (;;) {
+            for (int q = 0; q < d - 1; q++) memcpy(M + (size_t)q * d, psi + (size_t)c[q] * d, d);
+            memcpy(M + (size_t)(d - 1) * d, psi + (size_t)(i - 1) * d, d);
+            if (or_mat_rank(M, d, d) < d) { ok = 0; break; }
+            int q = d - 2;
+            while (q >= 0 && c[q] == (i - 1) - (d - 1) + q) q--;
+            if (q < 0) break;
+            c[q]++;
+            for (int r2 = q + 1; r2 < d - 1; r2++) c[r2] = c[r2 - 1] + 1;
+          }
+        }
+        if (ok) { lam[i - 1] = l; found = 1; }
+      }
+      if (!found) { free(lam); free(M); free(c); return OR_EUNSUP; }
+    }
+    if (lambda) memcpy(lambda, lam, n);
+    free(lam); free(M); free(c);
     return OR_OK;
   }
   if (kind == OR_MBR) {
@@ -490,7 +538,7 @@ int or_decode_msr_specific_Z(int kind, int n, int k, int d, const int *ids, cons
   int alpha, B;
   int rc = or_params(kind, n, k, d, &alpha, &B);
   if (rc) return rc;
-  if (kind != OR_MSR_SPARSE && kind != OR_MSR_VANILLA) return OR_EINVAL;
+  if (!OR_IS_MSR(kind)) return OR_EINVAL;
   for (int a = 0; a < k; a++) {
     if (ids[a] < 0 || ids[a] >= n) return OR_EINVAL;
     for (int b = 0; b < a; b++)
@@ -761,7 +809,7 @@ int or_validate(int kind, int n, int k, int d, long max_subsets, int check_phi, 
   rc = or_psi(kind, n, k, d, psi, lam);
   if (rc) { free(psi); free(lam); return rc; }
   int flags = 0;
-  if (kind == OR_MSR_SPARSE || kind == OR_MSR_VANILLA)
+  if (OR_IS_MSR(kind))
     for (int a = 0; a < n; a++)
       for (int b = 0; b < a; b++)
         if (lam[a] == lam[b]) flags |= 1;

@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpmrc.so")
 
-PMRC_MSR_SPARSE, PMRC_MSR_VANILLA, PMRC_MBR, PMRC_RS_VANDERMONDE = 0, 1, 2, 3
+PMRC_MSR_SPARSE, PMRC_MSR_VANILLA, PMRC_MBR, PMRC_RS_VANDERMONDE, PMRC_MSR_SPARSE_N2K = 0, 1, 2, 3, 4
 PMRC_OK, PMRC_EINVAL, PMRC_EUNSUPPORTED, PMRC_ESINGULAR = 0, -1, -2, -3
 PMRC_EALIGN, PMRC_ENOMEM, PMRC_ECUDA, PMRC_EJIT = -4, -5, -6, -7
 

@@ -45,6 +45,53 @@ bool all_subsets_full_rank(const Mat &psi, int rsel, int cols) {
   }
 }
 
+// Extension (not the paper's, R10b): the sparse Phi = [I; Cauchy] with
+// Lambda chosen greedily so that Psi stays valid at n = 2k: for nodes i = 0..n-1 in order,
+// lambda_i = g^e with the smallest e >= 0 such that lambda_i differs from the earlier lambdas and
+// every d-row subset of rows 0..i that contains row i has full rank.  Returns false if no e works.
+bool greedy_lambda(const Mat &phi, int n, int a, int d, Mat &psi, std::vector<uint8_t> &lambda) {
+  const GF256 &F = gf();
+  psi = Mat(n, d);
+  lambda.assign(n, 0);
+  Mat M(d, d);
+  for (int i = 0; i < n; i++) {
+    bool placed = false;
+    for (int e = 0; e < 255 && !placed; e++) {
+      const uint8_t lam = F.gexp(e);
+      bool clash = false;
+      for (int j = 0; j < i; j++) clash |= lambda[j] == lam;
+      if (clash) continue;
+      for (int t = 0; t < a; t++) {
+        psi.at(i, t) = phi.at(i, t);
+        psi.at(i, a + t) = F.mul(lam, phi.at(i, t));
+      }
+      bool ok = true;
+      if (i + 1 >= d) {
+        // subsets = row i plus every (d-1)-subset of rows 0..i-1
+        std::vector<int> c(d - 1);
+        for (int q = 0; q < d - 1; q++) c[q] = q;
+        for (;;) {
+          for (int q = 0; q < d - 1; q++)
+            for (int t = 0; t < d; t++) M.at(q, t) = psi.at(c[q], t);
+          for (int t = 0; t < d; t++) M.at(d - 1, t) = psi.at(i, t);
+          if (rank(M) < d) { ok = false; break; }
+          int q = d - 2;
+          while (q >= 0 && c[q] == i - (d - 1) + q) q--;
+          if (q < 0) break;
+          c[q]++;
+          for (int r = q + 1; r < d - 1; r++) c[r] = c[r - 1] + 1;
+        }
+      }
+      if (ok) {
+        lambda[i] = lam;
+        placed = true;
+      }
+    }
+    if (!placed) return false;
+  }
+  return true;
+}
+
 }  // namespace
 
 int build_code(int kind, int k, int d, int n, int w, CodeDef &o, std::string &err) {
@@ -56,6 +103,7 @@ int build_code(int kind, int k, int d, int n, int w, CodeDef &o, std::string &er
   switch (kind) {
     case KIND_MSR_SPARSE:
     case KIND_MSR_VANILLA:
+    case KIND_MSR_SPARSE_N2K:
       // alpha = Delta = d - k + 1; PM-MSR needs d = 2k - 2 (R7)
       if (k < 2 || d != 2 * k - 2) { err = "MSR requires k >= 2 and d = 2k-2"; return PMRC_EUNSUPPORTED; }
       if (n <= d) { err = "MSR requires n > d"; return PMRC_EINVAL; }
@@ -99,6 +147,19 @@ int build_code(int kind, int k, int d, int n, int w, CodeDef &o, std::string &er
             err = "vanilla MSR: Lambda values collide (n > 255/gcd(alpha,255), R8)";
             return PMRC_EUNSUPPORTED;
           }
+    } else if (kind == KIND_MSR_SPARSE_N2K) {
+      // extension: the paper's sparse Phi, greedy Lambda valid at n = 2k (greedy_lambda above)
+      if (n + a > 254) { err = "sparse MSR needs n + alpha <= 254 in GF(2^8)"; return PMRC_EUNSUPPORTED; }
+      if (n - 1 > 40) { err = "n=2k-valid sparse MSR: greedy Lambda search limited to n <= 41"; return PMRC_EUNSUPPORTED; }
+      Mat phi(n, a);
+      for (int i = 0; i < n; i++) {
+        uint8_t x = F.gexp(i + 1 + a);
+        for (int j = 0; j < a; j++) phi.at(i, j) = (i < a) ? (uint8_t)(i == j) : F.inv(x ^ F.gexp(j));
+      }
+      if (!greedy_lambda(phi, n, a, o.d, o.psi, o.lambda)) {
+        err = "n=2k-valid sparse MSR: no Lambda keeps every d-row subset invertible";
+        return PMRC_EUNSUPPORTED;
+      }
     } else if (kind == KIND_MSR_SPARSE) {
       // x_i = g^{i+alpha} (1-based i, R2); Phi = [I_alpha; 1/(x_i - y_j)], y_j = g^{j-1};
       // Lambda_ii = (x_i - 1)/(x_i - g^alpha)

@@ -9,7 +9,7 @@
 
 namespace pmrc {
 
-enum Kind { KIND_MSR_SPARSE = 0, KIND_MSR_VANILLA = 1, KIND_MBR = 2, KIND_RS = 3 };
+enum Kind { KIND_MSR_SPARSE = 0, KIND_MSR_VANILLA = 1, KIND_MBR = 2, KIND_RS = 3, KIND_MSR_SPARSE_N2K = 4 };
 
 struct CodeDef {
   int kind = 0, n = 0, k = 0, d = 0, alpha = 0, B = 0, P = 0;

@@ -67,4 +67,4 @@ class Stripes:
 
 def oracle_kind(kind):
     return {pm.PMRC_MSR_SPARSE: O.MSR_SPARSE, pm.PMRC_MSR_VANILLA: O.MSR_VANILLA, pm.PMRC_MBR: O.MBR,
-            pm.PMRC_RS_VANDERMONDE: O.RS}[kind]
+            pm.PMRC_RS_VANDERMONDE: O.RS, pm.PMRC_MSR_SPARSE_N2K: O.MSR_N2K}[kind]

@@ -22,7 +22,7 @@ def test_header_symbols_exported():
 
 
 @pytest.mark.parametrize("kind,k,n", [(0, 3, 6), (0, 8, 16), (1, 8, 16), (2, 8, 16), (3, 8, 16), (0, 4, 8), (2, 3, 6),
-                                      (0, 16, 32)])
+                                      (0, 16, 32), (4, 3, 6), (4, 8, 16)])
 def test_host_matrices_equal_oracle(kind, k, n):
     # the product's host construction (independent code) reproduces the oracle's matrices
     d = k if kind == 3 else 2 * k - 2

@@ -25,6 +25,7 @@ ENC_CASES = [
     (pm.PMRC_MBR, 4, 8, 1008, 4),
     (pm.PMRC_MSR_SPARSE, 16, 32, 1024 + 32, 1),
     (pm.PMRC_MSR_SPARSE, 2, 3, 16, 7),        # smallest code, one vector per block
+    (pm.PMRC_MSR_SPARSE_N2K, 8, 16, 2048 + 32, 2),   # R15 extension
 ]
 
 
@@ -149,7 +150,7 @@ def _predicted_singular(kind, k, n, f, H):
     return f < alpha and len(omitted) == 1 and omitted[0] < alpha
 
 
-@pytest.mark.parametrize("kind", [pm.PMRC_MSR_SPARSE, pm.PMRC_MSR_VANILLA, pm.PMRC_MBR])
+@pytest.mark.parametrize("kind", [pm.PMRC_MSR_SPARSE, pm.PMRC_MSR_VANILLA, pm.PMRC_MBR, pm.PMRC_MSR_SPARSE_N2K])
 def test_repair_config1_every_node_every_helper_set(kind):
     k, n, S, stripes = 3, 6, 2048, 16
     st = Stripes(kind, k, n, S, stripes, seed=1)
@@ -373,3 +374,28 @@ def test_per_stripe_patterns_one_launch_each():
             assert torch.equal(out[t], want[t]), t
     finally:
         st.close()
+
+
+def test_n2k_extension_repairs_paper_singular_sets_k8():
+    # R15: the (lost, helpers) pairs for which the paper's construction returns PMRC_ESINGULAR at
+    # k = 8, n = 16 (f < alpha, H omits another identity node) repair exactly with kind 4
+    k, n, S, stripes = 8, 16, 4096 + 16, 2
+    paper = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=71)
+    ext = Stripes(pm.PMRC_MSR_SPARSE_N2K, k, n, S, stripes, seed=71)
+    try:
+        ext.encode()
+        paper.encode()
+        for f, omit in ((0, 1), (3, 6), (6, 2)):
+            H = [i for i in range(n) if i not in (f, omit)]
+            out = torch.empty((stripes, ext.alpha, S), dtype=torch.uint8, device=DEV)
+            with pytest.raises(pm.PmrcError) as e:
+                pm.pmrc_repair(paper.code, f, H, [paper.piece(i) for i in H], (out.data_ptr(), paper.alpha * S), S,
+                               stripes, paper.stream)
+            assert e.value.rc == pm.PMRC_ESINGULAR
+            pm.pmrc_repair(ext.code, f, H, [ext.piece(i) for i in H], (out.data_ptr(), ext.alpha * S), S, stripes,
+                           ext.stream)
+            torch.cuda.synchronize()
+            assert torch.equal(out, ext.piece_tensor(f)), (f, H)
+    finally:
+        paper.close()
+        ext.close()

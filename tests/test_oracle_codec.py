@@ -76,7 +76,7 @@ def test_encode_gf_linearity():
 
 
 @pytest.mark.parametrize("kind,k,n", [(O.MSR_SPARSE, 3, 6), (O.MSR_VANILLA, 3, 6), (O.MBR, 3, 6),
-                                      (O.MSR_SPARSE, 4, 8), (O.MBR, 4, 8), (O.RS, 4, 8)])
+                                      (O.MSR_SPARSE, 4, 8), (O.MBR, 4, 8), (O.RS, 4, 8), (O.MSR_N2K, 4, 8)])
 def test_decode_every_k_subset(kind, k, n):
     # any k nodes recover the data; exhaustive over all k-subsets (and all larger sets at k=3)
     d = _d(kind, k)
@@ -147,7 +147,8 @@ def _sparse_n2k_singular(k, f, H, n):
 
 
 @pytest.mark.parametrize("kind,k,n", [(O.MSR_SPARSE, 3, 6), (O.MSR_VANILLA, 3, 6), (O.MSR_SPARSE, 4, 8),
-                                      (O.MSR_SPARSE, 3, 5), (O.MBR, 3, 6), (O.MBR, 4, 8)])
+                                      (O.MSR_SPARSE, 3, 5), (O.MBR, 3, 6), (O.MBR, 4, 8),
+                                      (O.MSR_N2K, 3, 6), (O.MSR_N2K, 4, 8)])
 def test_repair_every_node_every_helper_set(kind, k, n):
     # exact repair (P:53 fn): every lost node from every d-helper subset regenerates the
     # lost piece bit-exactly, except the predicted singular sets of the sparse code at n = 2k (R10)
@@ -258,3 +259,21 @@ def test_bruteforce_k2(kind, n):
     for f in range(n):
         for H in itertools.combinations([i for i in range(n) if i != f], d):
             assert (O.repair(kind, n, k, d, f, list(H), code[list(H)]) == code[f]).all()
+
+
+def test_n2k_extension_repairs_the_paper_singular_sets_at_k8():
+    # R15 (extension): with the greedy Lambda every (f, H) pair repairs exactly at k = 8, n = 16,
+    # including the 42 pairs that are singular for the paper's construction (R10)
+    k, n, d = 8, 16, 14
+    alpha, B = O.params(O.MSR_N2K, n, k, d)
+    X = _rand(B, 8)
+    code = O.full_code(O.MSR_N2K, n, k, d, X)
+    was_singular = 0
+    for f in range(n):
+        others = [i for i in range(n) if i != f]
+        for omit in others:
+            H = [i for i in others if i != omit]
+            was_singular += _sparse_n2k_singular(k, f, H, n)
+            got = O.repair(O.MSR_N2K, n, k, d, f, H, code[H])
+            assert (got == code[f]).all(), (f, H)
+    assert was_singular == 42

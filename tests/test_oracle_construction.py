@@ -218,3 +218,22 @@ def test_vanilla_lambda_collision():
         d = 2 * k - 2
         flags, _ = O.validate(O.MSR_VANILLA, 2 * k, k, d, check_phi=False, max_subsets=10 ** 5)
         assert not flags & 1, k
+
+
+@pytest.mark.parametrize("k", [3, 4, 8, 16])
+def test_n2k_extension_valid_and_sparse(k):
+    # R15 (extension, not the paper's): the sparse Phi = [I; Cauchy] with the greedy Lambda
+    # passes the P:121-127 constraints at n = 2k by brute force over every d-row subset (the
+    # paper's Lambda does not, R10), and keeps the systematic sparsity (k-2)/k of Table 1
+    d, n = 2 * k - 2, 2 * k
+    flags, _ = O.validate(O.MSR_N2K, n, k, d, check_phi=(k <= 8))
+    assert flags == 0
+    assert O.validate(O.MSR_SPARSE, n, k, d, check_phi=False)[0] & 2
+    G2 = O.parity_matrix(O.MSR_N2K, n, k, d)
+    assert (G2 == 0).mean() >= (k - 2) / k
+    P, lam = O.psi(O.MSR_N2K, n, k, d)
+    Ps, _ = O.psi(O.MSR_SPARSE, n, k, d)
+    alpha = k - 1
+    assert (P[:, :alpha] == Ps[:, :alpha]).all()        # same Phi as the paper's sparse code
+    for i in range(n):                                     # Psi = [Phi  Lambda Phi]
+        assert all(P[i, alpha + j] == O.gf_mul(lam[i], P[i, j]) for j in range(alpha))

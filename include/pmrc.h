@@ -97,7 +97,8 @@ void pmrc_destroy(pmrc_code *c);
 int pmrc_info(const pmrc_code *c, pmrc_info_t *out);
 
 /* Copy matrices out (host memory).  which: 0 = Psi (n x d; RS n x k), 1 = G (n alpha x B),
- * 2 = G' (n alpha x B), 3 = G'' (parity_rows x B), 4 = lambda (n).  rows/cols receive the shape;
+ * 2 = G' (n alpha x B), 3 = G'' (parity_rows x B), 4 = lambda (n), 5 = Gtilde^{-1} (B x B, the
+ * precode of P:112; MSR / RS only, PMRC_EUNSUPPORTED for MBR).  rows/cols receive the shape;
  * buf may be NULL to query the shape; otherwise it must hold rows*cols bytes. */
 int pmrc_matrix(const pmrc_code *c, int which, uint8_t *buf, int *rows, int *cols);
 /* Index matrix L, 1-based data indices, 0 = structural zero: MSR d x alpha, MBR d x d,
@@ -109,8 +110,8 @@ int pmrc_layout(const pmrc_code *c, int *buf, int *rows, int *cols);
 int pmrc_encode(pmrc_code *c, const void *data, void *parity, size_t S, size_t stripes, void *stream);
 
 /* Same computation from HOST buffers (pinned memory recommended): the library stages chunks of
- * stripes through device buffers it owns (2 x chunk), overlapping H2D, the encode kernel and D2H
- * on `stream` plus an internal copy stream.  Synchronises before returning. */
+ * stripes through a ring of 3 device buffers it owns, overlapping H2D, the encode kernel and D2H on
+ * 3 internal streams ordered after `stream`.  Synchronises before returning. */
 int pmrc_encode_host(pmrc_code *c, const void *data_host, void *parity_host, size_t S, size_t stripes,
                      void *stream);
 
@@ -138,6 +139,16 @@ int pmrc_repair_project(pmrc_code *c, int lost_id, pmrc_cregion piece, pmrc_regi
 /* newcomer: out_piece from the d helpers' betas (betas[i] belongs to helper_ids[i]). */
 int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers, const pmrc_cregion *betas,
                         pmrc_region out_piece, size_t S, size_t stripes, void *stream);
+
+/* General region linear combination on the same generated kernels: for every stripe t and byte
+ * position, out block r = XOR_c A[r][c] * in block c (GF(2^8), r < rows, c < cols), with input
+ * block c of stripe t at in + t*in_stride + c*S and output block r at out + t*out_stride + r*S.
+ * A: rows x cols, row-major, host memory; zero coefficients are skipped at generation time.  The
+ * kernel is generated per matrix and cached on the handle (keyed by shape + coefficient hash).
+ * Used for the paper's comparison paths (non-systematic encode Y = G Z, precode Z = Gtilde^{-1} X
+ * then parity = G_parity Z).  PMRC_EINVAL for an all-zero A. */
+int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *in, size_t in_stride, void *out,
+               size_t out_stride, size_t S, size_t stripes, void *stream);
 
 /* Blocks each helper reads to repair lost_id: nnz(phi_f) (MSR: 1 if f < alpha else alpha,
  * P:209), nnz(psi_f) for MBR, 1 for RS. */
@@ -172,6 +183,8 @@ typedef struct {
   int transposes;
 } pmrc_plan_stats_t;
 int pmrc_plan_stats(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids, pmrc_plan_stats_t *out);
+/* The same for the plan pmrc_apply would run for matrix A (rows x cols). */
+int pmrc_apply_stats(pmrc_code *c, const uint8_t *A, int rows, int cols, pmrc_plan_stats_t *out);
 
 /* Diagnostics of the encode kernel's CTA pacing (group-specialised layout): copies the device
  * counter area (5 x E u64: progress counters, then per-(CTA, team) start / end globaltimer ns, ns

@@ -16,12 +16,12 @@ PMRC_MSR_SPARSE, PMRC_MSR_VANILLA, PMRC_MBR, PMRC_RS_VANDERMONDE, PMRC_MSR_SPARS
 PMRC_OK, PMRC_EINVAL, PMRC_EUNSUPPORTED, PMRC_ESINGULAR = 0, -1, -2, -3
 PMRC_EALIGN, PMRC_ENOMEM, PMRC_ECUDA, PMRC_EJIT = -4, -5, -6, -7
 
-MATRIX_PSI, MATRIX_G, MATRIX_GSYS, MATRIX_GPP, MATRIX_LAMBDA = 0, 1, 2, 3, 4
+MATRIX_PSI, MATRIX_G, MATRIX_GSYS, MATRIX_GPP, MATRIX_LAMBDA, MATRIX_GTINV = 0, 1, 2, 3, 4, 5
 
 EXPORTS = ["pmrc_create", "pmrc_destroy", "pmrc_info", "pmrc_matrix", "pmrc_layout", "pmrc_encode",
            "pmrc_encode_host", "pmrc_decode", "pmrc_repair", "pmrc_repair_project", "pmrc_repair_combine",
            "pmrc_read_cost", "pmrc_launch_count", "pmrc_strerror", "pmrc_last_error", "pmrc_precompile",
-           "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source", "pmrc_plan_stats"]
+           "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source", "pmrc_plan_stats", "pmrc_apply", "pmrc_apply_stats"]
 
 
 class PmrcError(RuntimeError):
@@ -84,6 +84,8 @@ def lib():
             "pmrc_debug_counters": ([P, P, Z, ctypes.POINTER(ctypes.c_size_t)], I),
             "pmrc_plan_source": ([P, I, I, IP, I, I, P, Z, ctypes.POINTER(ctypes.c_size_t)], I),
             "pmrc_plan_stats": ([P, I, I, IP, I, ctypes.POINTER(pmrc_plan_stats_t)], I),
+            "pmrc_apply": ([P, P, I, I, P, Z, P, Z, Z, Z, P], I),
+            "pmrc_apply_stats": ([P, P, I, I, ctypes.POINTER(pmrc_plan_stats_t)], I),
             "pmrc_strerror": ([I], ctypes.c_char_p),
             "pmrc_last_error": ([], ctypes.c_char_p),
         }
@@ -210,6 +212,24 @@ def pmrc_plan_source(code, op, lost_id, ids, compile=False):
     _check(lib().pmrc_plan_source(code, op, lost_id, arr, len(ids), 0, buf, n.value + 1, ctypes.byref(n)),
            "pmrc_plan_source")
     return buf.value.decode()
+
+
+def pmrc_apply(code, A, in_ptr, in_stride, out_ptr, out_stride, S, stripes, stream=0):
+    """out block r = XOR_c A[r][c] * in block c for every stripe (A: host uint8 rows x cols)."""
+    import numpy as np
+    A = np.ascontiguousarray(A, dtype=np.uint8)
+    rows, cols = A.shape
+    _check(lib().pmrc_apply(code, A.ctypes.data, rows, cols, in_ptr, in_stride, out_ptr, out_stride, S, stripes,
+                            stream), "pmrc_apply")
+
+
+def pmrc_apply_stats(code, A):
+    """Per-stripe work of the pmrc_apply plan for matrix A."""
+    import numpy as np
+    A = np.ascontiguousarray(A, dtype=np.uint8)
+    st = pmrc_plan_stats_t()
+    _check(lib().pmrc_apply_stats(code, A.ctypes.data, A.shape[0], A.shape[1], ctypes.byref(st)), "pmrc_apply_stats")
+    return {f: getattr(st, f) for f, _ in pmrc_plan_stats_t._fields_}
 
 
 def pmrc_plan_stats(code, op, lost_id=0, ids=()):

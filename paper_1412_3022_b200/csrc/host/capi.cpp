@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -342,6 +343,20 @@ int pmrc_plan_source(pmrc_code *c, int op, int lost_id, const int *ids, int n_id
   return PMRC_OK;
 }
 
+static void fill_stats(const PlanSpec &spec, const GenStats &st, pmrc_plan_stats_t *out);
+
+int pmrc_apply_stats(pmrc_code *c, const uint8_t *A, int rows, int cols, pmrc_plan_stats_t *out) {
+  if (!c || !out || !A) return fail(PMRC_EINVAL, "NULL argument");
+  memset(out, 0, sizeof(*out));
+  std::string src;
+  c->dry = &src;
+  int rc = pmrc_apply(c, A, rows, cols, (const void *)(uintptr_t)4096, 0, (void *)(uintptr_t)4096, 0, 16, 0, nullptr);
+  c->dry = nullptr;
+  if (rc != kDryRun) return rc ? rc : fail(PMRC_EINVAL, "no kernel for this matrix");
+  fill_stats(c->dry_spec, c->dry_stats, out);
+  return PMRC_OK;
+}
+
 int pmrc_plan_stats(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids, pmrc_plan_stats_t *out) {
   if (!c || !out) return fail(PMRC_EINVAL, "NULL argument");
   memset(out, 0, sizeof(*out));
@@ -356,6 +371,11 @@ int pmrc_plan_stats(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids
     st = c->dry_stats;
     spec = c->dry_spec;
   }
+  fill_stats(spec, st, out);
+  return PMRC_OK;
+}
+
+static void fill_stats(const PlanSpec &spec, const GenStats &st, pmrc_plan_stats_t *out) {
   std::vector<std::pair<int, int>> blocks;
   for (auto &in : spec.inputs)
     for (auto &t : in.terms) blocks.push_back({t.slot, t.blk});
@@ -367,7 +387,6 @@ int pmrc_plan_stats(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids
   out->naive_lop3 = st.naive_lop3;
   out->xor2 = st.xor2;
   out->transposes = st.transposes;
-  return PMRC_OK;
 }
 
 int pmrc_encode_source(const pmrc_code *c, char *buf, size_t cap, size_t *len) {
@@ -393,6 +412,10 @@ int pmrc_matrix(const pmrc_code *c, int which, uint8_t *buf, int *rows, int *col
     case 1: M = &D.G; break;
     case 2: M = &D.Gsys; break;
     case 3: M = &D.Gpp; break;
+    case 5:
+      if (D.Gti.r == 0) return fail(PMRC_EUNSUPPORTED, "MBR has no precode matrix (its systematic rows are unit rows)");
+      M = &D.Gti;
+      break;
     case 4:
       lam = Mat(1, D.n);
       for (int i = 0; i < D.n && i < (int)D.lambda.size(); i++) lam.at(0, i) = D.lambda[i];
@@ -595,6 +618,46 @@ int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregio
   strides[n_surv] = (uint64_t)D.B * S;
   std::string err;
   rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err);
+  if (rc) return fail(rc, err);
+  return PMRC_OK;
+}
+
+int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *in, size_t in_stride, void *out,
+               size_t out_stride, size_t S, size_t stripes, void *stream) {
+  if (!c || !A || !in || !out) return fail(PMRC_EINVAL, "NULL argument");
+  if (rows < 1 || cols < 1 || rows > 4096 || cols > 4096) return fail(PMRC_EINVAL, "bad matrix shape");
+  if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
+  // plan key: shape + FNV-1a of the coefficients (the matrix defines the kernel)
+  uint64_t h = 1469598103934665603ull;
+  for (long i = 0; i < (long)rows * cols; i++) h = (h ^ A[i]) * 1099511628211ull;
+  char kb[96];
+  snprintf(kb, sizeof kb, "apply:%dx%d:%016llx", rows, cols, (unsigned long long)h);
+  const std::string key = kb;
+  Kernel *K = nullptr;
+  auto it = c->plans.find(key);
+  if (c->dry || it == c->plans.end()) {
+    PlanSpec spec;
+    spec.n_slots = 2;
+    for (int x = 0; x < cols; x++) spec.inputs.push_back({{{0, x, 1}}});
+    for (int r = 0; r < rows; r++) spec.outputs.push_back({1, r});
+    spec.A = Mat(rows, cols);
+    memcpy(spec.A.a.data(), A, (size_t)rows * cols);
+    bool any = false;
+    for (uint8_t v : spec.A.a) any |= v != 0;
+    if (!any) return fail(PMRC_EINVAL, "all-zero matrix (nothing to compute)");
+    int rc = get_kernel(c, key, spec, &K);
+    if (rc) return rc;
+  } else {
+    K = it->second.get();
+  }
+  if (!stripes || !S) return PMRC_OK;
+  int rc = check_region(in, in_stride, stripes);
+  if (!rc) rc = check_region(out, out_stride, stripes);
+  if (rc) return fail(rc, "bad in/out region");
+  uint64_t ptrs[2] = {(uint64_t)(uintptr_t)in, (uint64_t)(uintptr_t)out};
+  uint64_t strides[2] = {(uint64_t)in_stride, (uint64_t)out_stride};
+  std::string err;
+  rc = launch_kernel(*K, ptrs, strides, S, stripes, stream, err);
   if (rc) return fail(rc, err);
   return PMRC_OK;
 }

@@ -231,6 +231,7 @@ int build_code(int kind, int k, int d, int n, int w, CodeDef &o, std::string &er
       for (int c2 = 0; c2 < o.B; c2++) Gt.at(r, c2) = o.G.at(r, c2);
     if (!invert(Gt, Gti)) { err = "Gtilde (first B rows of G) is singular"; return PMRC_EUNSUPPORTED; }
     o.Gsys = matmul(o.G, Gti);
+    o.Gti = Gti;
   }
   o.Gpp = Mat(o.P, o.B);
   for (int r = 0; r < o.P; r++)

@@ -21,6 +21,7 @@ struct CodeDef {
   Mat G;     // n alpha x B
   Mat Gsys;  // G'
   Mat Gpp;   // P x B
+  Mat Gti;   // Gtilde^{-1} (B x B; MSR / RS), the precode of P:112
   bool repair_complete = true;
 
   // data block held by systematic node i, symbol j (MSR/RS: i*alpha+j; MBR: L_{i,j}-1)

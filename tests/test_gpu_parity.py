@@ -399,3 +399,35 @@ def test_n2k_extension_repairs_paper_singular_sets_k8():
     finally:
         paper.close()
         ext.close()
+
+
+def test_apply_matches_encode_specific_and_precode_paths():
+    # pmrc_apply (general region linear combination) on the paper's comparison paths:
+    #  * non-systematic encode Y = G Z equals the oracle's specific PM encode C = Psi M(Z)
+    #  * precode Z = Gtilde^{-1} X, then parity = G_parity Z, equals the linearised systematic
+    #    encode G'' X (the two systematic encoders give identical codewords)
+    k, n, S, stripes = 8, 16, 2048 + 48, 2
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=81)
+    try:
+        st.encode()
+        G = pm.pmrc_matrix(st.code, pm.MATRIX_G)
+        Gti = pm.pmrc_matrix(st.code, pm.MATRIX_GTINV)
+        B, a = st.B, st.alpha
+        Y = torch.empty((stripes, n * a, S), dtype=torch.uint8, device=DEV)
+        pm.pmrc_apply(st.code, G, st.data.data_ptr(), B * S, Y.data_ptr(), n * a * S, S, stripes, st.stream)
+        torch.cuda.synchronize()
+        Z = st.host_data()
+        want = np.stack([O.encode_specific(O.MSR_SPARSE, n, k, st.d, Z[t]).reshape(n * a, S) for t in range(stripes)])
+        assert np.array_equal(Y.cpu().numpy(), want)
+        Zd = torch.empty_like(st.data)
+        pm.pmrc_apply(st.code, Gti, st.data.data_ptr(), B * S, Zd.data_ptr(), B * S, S, stripes, st.stream)
+        par = torch.empty_like(st.parity)
+        pm.pmrc_apply(st.code, G[k * a:], Zd.data_ptr(), B * S, par.data_ptr(), st.P * S, S, stripes, st.stream)
+        torch.cuda.synchronize()
+        assert torch.equal(par, st.parity)
+        Gpp = pm.pmrc_matrix(st.code, pm.MATRIX_GPP)
+        pm.pmrc_apply(st.code, Gpp, st.data.data_ptr(), B * S, par.data_ptr(), st.P * S, S, stripes, st.stream)
+        torch.cuda.synchronize()
+        assert torch.equal(par, st.parity)
+    finally:
+        st.close()

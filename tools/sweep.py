@@ -274,6 +274,39 @@ def main():
         for _ in range(2):
             run_repair(j, rng, args.steps, "next1-mbr")
         j.close()
+    if "next2" in cfgs:
+        # the linearised systematic encode vs the paper's other
+        # encoders on the same kernels through pmrc_apply: non-systematic Y = G Z (the specific PM
+        # encode C = Psi M), and precode-then-encode (Z = Gtilde^-1 X, parity = G_parity Z)
+        for kind in (MSR, VAN):
+            j = run_encode(kind, 8, 16, 1 << 20, args.steps)
+            G = pm.pmrc_matrix(j.code, pm.MATRIX_G)
+            Gti = pm.pmrc_matrix(j.code, pm.MATRIX_GTINV)
+            na = j.n * j.alpha
+            Y = torch.empty((j.stripes, na, j.S), dtype=torch.uint8, device="cuda")
+            Z = torch.empty_like(j.data)
+            par = torch.empty_like(j.par)
+            S, st = j.S, j.st
+
+            def nonsys():
+                pm.pmrc_apply(j.code, G, j.data.data_ptr(), j.B * S, Y.data_ptr(), na * S, S, j.stripes, st)
+
+            def precode():
+                pm.pmrc_apply(j.code, Gti, j.data.data_ptr(), j.B * S, Z.data_ptr(), j.B * S, S, j.stripes, st)
+                pm.pmrc_apply(j.code, G[j.k * j.alpha:], Z.data_ptr(), j.B * S, par.data_ptr(), j.P * S, S, j.stripes,
+                              st)
+            precode()
+            torch.cuda.synchronize()
+            ok = bool(torch.equal(par, j.par))
+            src = j.stripes * j.B * S
+            for name, fn, mats in (("encode_nonsystematic", nonsys, [G]), ("precode_then_encode", precode,
+                                                                             [Gti, G[j.k * j.alpha:]])):
+                ms = timed(fn, args.steps)
+                naive = sum(pm.pmrc_apply_stats(j.code, m)["naive_lop3"] for m in mats)
+                emit({"op": name, "config": "next2", "kind": KIND_NAMES[kind], "k": 8, "n": 16, "S": S,
+                      "ms": round(ms, 4), "GBps": round(src / ms / 1e6, 1), "naive_lop3_per_32pos": naive,
+                      "bit_exact": ok if name == "precode_then_encode" else None})
+            j.close()
     if "5" in cfgs:
         for kind in (MSR, MBR):
             for k in [int(x) for x in args.ks.split(",")]:

@@ -431,3 +431,31 @@ def test_apply_matches_encode_specific_and_precode_paths():
         assert torch.equal(par, st.parity)
     finally:
         st.close()
+
+
+def test_decode_and_repair_write_only_their_outputs():
+    # no compute-sanitizer on this pool: bounds by sentinels instead.  Decode writes exactly the
+    # missing data blocks (every other byte of data_out keeps its sentinel); repair writes exactly
+    # stripes x alpha x S bytes (guard bytes after the piece stay intact); ragged S
+    k, n, S, stripes = 8, 16, 3072 + 16, 3
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=91)
+    try:
+        st.encode()
+        ids = [1, 2, 5, 6, 9, 10, 13, 15]
+        out = torch.full_like(st.data, 0xA5)
+        nw = pm.pmrc_decode(st.code, ids, [st.piece(i) for i in ids], out.data_ptr(), S, stripes, st.stream)
+        torch.cuda.synchronize()
+        miss = [i * st.alpha + a for i in range(k) if i not in ids for a in range(st.alpha)]
+        keep = [b for b in range(st.B) if b not in miss]
+        assert nw == len(miss)
+        assert torch.equal(out[:, miss], st.data[:, miss])
+        assert bool((out[:, keep] == 0xA5).all())
+        f, H = 12, [i for i in range(n) if i not in (12, 4)]
+        big = torch.full((stripes * st.alpha * S + 8192,), 0x3C, dtype=torch.uint8, device=DEV)
+        pm.pmrc_repair(st.code, f, H, [st.piece(i) for i in H], (big.data_ptr(), st.alpha * S), S, stripes,
+                       st.stream)
+        torch.cuda.synchronize()
+        assert bool((big[stripes * st.alpha * S:] == 0x3C).all())
+        assert torch.equal(big[: stripes * st.alpha * S].view(stripes, st.alpha, S), st.piece_tensor(f))
+    finally:
+        st.close()

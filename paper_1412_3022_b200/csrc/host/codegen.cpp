@@ -725,7 +725,8 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         // consume: own copies landed -> transpose own share -> team barrier
         s << "          pm_cp_wait<" << (D - 1) << ">();\n";
         s << "          const u32 buf = sbuf + pb * (PM_QMAX * 1024u);\n";
-        s << "          pm_transpose_in(buf + lane * 16u, " << nblk * rk / T << "u, " << nblk * (rk + 1) / T << "u);\n";
+        if (!(o.debug & 1))  // debug bit 0: skip the input transposes (timing experiments only: wrong results)
+          s << "          pm_transpose_in(buf + lane * 16u, " << nblk * rk / T << "u, " << nblk * (rk + 1) / T << "u);\n";
         s << "          const u32 pl = buf + lane * 16u;\n";
         // the team barrier + the prefetch of the successor stage into the other buffer; emitted
         // after the sub-networks that read only this warp's own transposed blocks (below)
@@ -882,6 +883,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
       for (int r = 0; r < m; r++) {
         const OutputDesc &od = p.outputs[G.rows[r0 + r]];
         std::string n = "o" + std::to_string(r);
+        if (!(o.debug & 2))  // debug bit 1: skip the output transposes (timing experiments only)
         s << "        pm_tr8(" << n << "_0, " << n << "_1, " << n << "_2, " << n << "_3, " << n << "_4, " << n << "_5, "
           << n << "_6, " << n << "_7);\n";
         s << "        { unsigned char *pp = (unsigned char *)(ob" << od.slot << " + (u64)" << od.blk << "u * S);\n";

@@ -236,6 +236,7 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "nbuf" && v >= 2) c->gen.nbuf = v;
         if (key == "own_first") c->gen.own_first = v != 0;
         if (key == "debug") c->gen.debug = v;
+        if (key == "l2_shared") c->gen.l2_shared = v;
         if (key == "grid_ctas" && v > 0) c->gen.grid_ctas = v;
       }
       pos = e + 1;

@@ -76,6 +76,11 @@ static __device__ __forceinline__ void pm_cp16(u32 dst, const void *src, u32 src
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;"
                :: "r"(dst), "l"(src), "r"(src_size), "l"(pol) : "memory");
 }
+static __device__ __forceinline__ u64 pm_policy_el() {
+  u64 p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 static __device__ __forceinline__ u64 pm_policy_en() {
   u64 p;
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
@@ -559,9 +564,23 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     for (size_t g = 0; g < groups.size(); g++)
       for (int si : gstages[g])
         for (size_t i = 0; i < stages[si].blocks.size(); i++) last[stages[si].blocks[i]] = {si, (int)i};
+    // layouts 1/2 run the groups concurrently on different SMs, so "the last read" is not known
+    // statically there: a block loaded by more than one group gets policy o.l2_shared (0 normal,
+    // 2 evict_last), a block loaded by one group only is streamed with evict_first
+    std::map<std::pair<int, int>, int> readers;
+    for (size_t g = 0; g < groups.size(); g++) {
+      std::map<std::pair<int, int>, bool> seen;
+      for (int si : gstages[g])
+        for (auto &b : stages[si].blocks) seen[b] = true;
+      for (auto &kv : seen) readers[kv.first]++;
+    }
     for (size_t si = 0; si < stages.size(); si++) {
       stages[si].ef.assign(stages[si].blocks.size(), 0);
       for (size_t i = 0; i < stages[si].blocks.size(); i++) {
+        if (o.layout >= 1 && o.l2_shared >= 0) {
+          stages[si].ef[i] = readers[stages[si].blocks[i]] > 1 ? (o.l2_shared == 2 ? 2 : 0) : 1;
+          continue;
+        }
         auto l = last[stages[si].blocks[i]];
         stages[si].ef[i] = (l.first == (int)si && l.second == (int)i) ? 1 : 0;
       }
@@ -651,10 +670,11 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         const auto &bk = sg.blocks[i];
         o2 << ind << "    { const u64 a = sb" << bk.first << " + (u64)" << bk.second << "u * S;\n";
         // src_size 0 (chunk beyond S) zero-fills without reading the source
-        o2 << ind << "      pm_cp16(dst + " << i * 1024 << "u, (const void *)a, z0, " << (sg.ef[i] ? "pol_ef" : "pol_en")
+        const char *pol = sg.ef[i] == 1 ? "pol_ef" : (sg.ef[i] == 2 ? "pol_el" : "pol_en");
+        o2 << ind << "      pm_cp16(dst + " << i * 1024 << "u, (const void *)a, z0, " << pol
            << ");\n";
         o2 << ind << "      pm_cp16(dst + " << i * 1024 + 512 << "u, (const void *)(a + 512u), z1, "
-           << (sg.ef[i] ? "pol_ef" : "pol_en") << "); }\n";
+           << pol << "); }\n";
       }
       o2 << ind << "  } break;\n";
     }
@@ -904,7 +924,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   s << "  const u32 per_cta = (total + gridDim.x - 1u) / gridDim.x;\n";
   s << "  const u32 c0 = blockIdx.x * per_cta, c1 = min(total, c0 + per_cta);\n";
   s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (" << NB << "u * PM_QMAX * 1024u);\n";
-  s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en();\n";
+  s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en(), pol_el = pm_policy_el();\n";
   s << "  u32 pb = 0u;\n";
   if (first_sid >= 0) {
     s << "  if (c0 < c1) {\n";
@@ -960,7 +980,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   // Teams interleave over the range (team, team + teams, ...) so all groups advance in step.
   s << "  const u32 teams = " << teams << "u;\n";
   s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (" << NB << "u * PM_QMAX * 1024u);\n";
-  s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en();\n";
+  s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en(), pol_el = pm_policy_el();\n";
   s << "  u32 pb = 0u;\n";
   s << "  bool pacing = pace != 0;\n";
   if (o.trace) s << "  const u64 tr_t0 = pm_gtime(); u64 tr_wait = 0; u32 tr_fail = 0;\n";

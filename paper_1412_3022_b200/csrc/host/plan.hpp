@@ -54,6 +54,7 @@ struct GenOptions {
   bool auto_wide = true;    // resolve_options: 16-row groups on 4-warp teams for wide multi-stage plans
   int cse_restarts = 1;     // CSE runs per network (seeded near-tie randomisation), keep the cheapest
   bool sched = false;       // register-pressure-aware temp order (emit_slp_sched) instead of CSE order
+  int l2_shared = 0;        // layouts 1/2: L2 policy of blocks read by >1 group (-1 static last-read rule, 0 normal, 2 evict_last)
   int debug = 0;            // timing experiments only (wrong results): 1 skip input, 2 skip output transposes
   bool own_first = false;   // sub-networks over a warp's own transposed blocks before the team barrier
   int nbuf = 2;             // stage buffers per team (layouts 1/2): prefetch nbuf-1 stages ahead

@@ -150,6 +150,12 @@ int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids, int n_
 int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *in, size_t in_stride, void *out,
                size_t out_stride, size_t S, size_t stripes, void *stream);
 
+/* Cap the grid of every launch on this handle at max_ctas CTAs (0 = default: one full wave, one
+ * persistent CTA per SM).  With a cap, small launches issued on several streams (e.g. config 4's
+ * per-stripe failure patterns, one plan per stripe) run side by side on disjoint SMs instead of
+ * each paying a full-GPU ramp and tail. */
+int pmrc_set_max_ctas(pmrc_code *c, int max_ctas);
+
 /* Blocks each helper reads to repair lost_id: nnz(phi_f) (MSR: 1 if f < alpha else alpha,
  * P:209), nnz(psi_f) for MBR, 1 for RS. */
 int pmrc_read_cost(const pmrc_code *c, int lost_id, int *blocks_per_helper);

@@ -21,7 +21,7 @@ MATRIX_PSI, MATRIX_G, MATRIX_GSYS, MATRIX_GPP, MATRIX_LAMBDA, MATRIX_GTINV = 0, 
 EXPORTS = ["pmrc_create", "pmrc_destroy", "pmrc_info", "pmrc_matrix", "pmrc_layout", "pmrc_encode",
            "pmrc_encode_host", "pmrc_decode", "pmrc_repair", "pmrc_repair_project", "pmrc_repair_combine",
            "pmrc_read_cost", "pmrc_launch_count", "pmrc_strerror", "pmrc_last_error", "pmrc_precompile",
-           "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source", "pmrc_plan_stats", "pmrc_apply", "pmrc_apply_stats"]
+           "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source", "pmrc_plan_stats", "pmrc_apply", "pmrc_apply_stats", "pmrc_set_max_ctas"]
 
 
 class PmrcError(RuntimeError):
@@ -86,6 +86,7 @@ def lib():
             "pmrc_plan_stats": ([P, I, I, IP, I, ctypes.POINTER(pmrc_plan_stats_t)], I),
             "pmrc_apply": ([P, P, I, I, P, Z, P, Z, Z, Z, P], I),
             "pmrc_apply_stats": ([P, P, I, I, ctypes.POINTER(pmrc_plan_stats_t)], I),
+            "pmrc_set_max_ctas": ([P, I], I),
             "pmrc_strerror": ([I], ctypes.c_char_p),
             "pmrc_last_error": ([], ctypes.c_char_p),
         }
@@ -221,6 +222,11 @@ def pmrc_apply(code, A, in_ptr, in_stride, out_ptr, out_stride, S, stripes, stre
     rows, cols = A.shape
     _check(lib().pmrc_apply(code, A.ctypes.data, rows, cols, in_ptr, in_stride, out_ptr, out_stride, S, stripes,
                             stream), "pmrc_apply")
+
+
+def pmrc_set_max_ctas(code, max_ctas):
+    """Grid cap for every launch on this handle (0 = one full wave)."""
+    _check(lib().pmrc_set_max_ctas(code, max_ctas), "pmrc_set_max_ctas")
 
 
 def pmrc_apply_stats(code, A):

@@ -48,6 +48,7 @@ struct pmrc_code {
   std::map<std::string, int> plan_err;                   // cached failures (ESINGULAR)
   std::map<std::string, int> plan_meta;                  // e.g. blocks written by a decode plan
   HostStage hs;
+  int max_ctas = 0;            // pmrc_set_max_ctas: grid cap for every launch (0 = one full wave)
   std::string *dry = nullptr;  // pmrc_plan_source: get_kernel stores the generated source here instead
   PlanSpec dry_spec;           //   and the plan
   GenStats dry_stats;
@@ -452,7 +453,7 @@ int pmrc_encode(pmrc_code *c, const void *data, void *parity, size_t S, size_t s
   uint64_t ptrs[2] = {(uint64_t)(uintptr_t)data, (uint64_t)(uintptr_t)parity};
   uint64_t strides[2] = {(uint64_t)D.B * S, (uint64_t)D.P * S};
   std::string err;
-  rc = launch_kernel(c->enc, ptrs, strides, S, stripes, stream, err);
+  rc = launch_kernel(c->enc, ptrs, strides, S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
   return PMRC_OK;
 }
@@ -501,7 +502,7 @@ int pmrc_encode_host(pmrc_code *c, const void *data_host, void *parity_host, siz
     uint64_t ptrs[2] = {(uint64_t)(uintptr_t)h.d_data[b], (uint64_t)(uintptr_t)h.d_par[b]};
     uint64_t strides[2] = {in_b, out_b};
     std::string err;
-    rc = launch_kernel(c->enc, ptrs, strides, S, ns, st, err);
+    rc = launch_kernel(c->enc, ptrs, strides, S, ns, st, err, c->max_ctas);
     if (rc) return fail(rc, err);
     if (cudaMemcpyAsync((uint8_t *)parity_host + s0 * out_b, h.d_par[b], ns * out_b, cudaMemcpyDeviceToHost, st) !=
         cudaSuccess)
@@ -619,7 +620,7 @@ int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregio
   ptrs[n_surv] = (uint64_t)(uintptr_t)data_out;
   strides[n_surv] = (uint64_t)D.B * S;
   std::string err;
-  rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err);
+  rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
   return PMRC_OK;
 }
@@ -659,8 +660,14 @@ int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *i
   uint64_t ptrs[2] = {(uint64_t)(uintptr_t)in, (uint64_t)(uintptr_t)out};
   uint64_t strides[2] = {(uint64_t)in_stride, (uint64_t)out_stride};
   std::string err;
-  rc = launch_kernel(*K, ptrs, strides, S, stripes, stream, err);
+  rc = launch_kernel(*K, ptrs, strides, S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
+  return PMRC_OK;
+}
+
+int pmrc_set_max_ctas(pmrc_code *c, int max_ctas) {
+  if (!c || max_ctas < 0) return fail(PMRC_EINVAL, "bad argument");
+  c->max_ctas = max_ctas;
   return PMRC_OK;
 }
 
@@ -732,7 +739,7 @@ int pmrc_repair(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers,
   ptrs[n_helpers] = (uint64_t)(uintptr_t)out_piece.ptr;
   strides[n_helpers] = out_piece.stripe_stride;
   std::string err;
-  rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err);
+  rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
   return PMRC_OK;
 }
@@ -770,7 +777,7 @@ int pmrc_repair_project(pmrc_code *c, int lost_id, pmrc_cregion piece, pmrc_regi
   uint64_t ptrs[2] = {(uint64_t)(uintptr_t)piece.ptr, (uint64_t)(uintptr_t)beta.ptr};
   uint64_t strides[2] = {piece.stripe_stride, beta.stripe_stride};
   std::string err;
-  rc = launch_kernel(*K, ptrs, strides, S, stripes, stream, err);
+  rc = launch_kernel(*K, ptrs, strides, S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
   return PMRC_OK;
 }
@@ -816,7 +823,7 @@ int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids, int n_
   ptrs[n_helpers] = (uint64_t)(uintptr_t)out_piece.ptr;
   strides[n_helpers] = out_piece.stripe_stride;
   std::string err;
-  rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err);
+  rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
   return PMRC_OK;
 }

@@ -242,7 +242,7 @@ void free_kernel(Kernel &k) {
 static int oo_grid(const Kernel &k) { return k.grid_ctas; }
 
 int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides, size_t S, size_t stripes,
-                  void *stream, std::string &err) {
+                  void *stream, std::string &err, int max_ctas) {
   if (S == 0 || stripes == 0) return PMRC_OK;
   const uint64_t chunks64 = (S + 1023) / 1024;
   if (chunks64 > 0xFFFFFFFFull) { err = "S too large"; return PMRC_EINVAL; }
@@ -260,8 +260,10 @@ int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides
     uint64_t S64 = S;
     // the kernel splits the ns * chunks chunk range evenly over the CTAs
     uint64_t grid = (uint64_t)k.sms * k.blocks_per_sm;
+    // a grid cap lets several small launches (per-stripe failure patterns) share the GPU
+    if (max_ctas > 0) grid = std::min<uint64_t>(grid, (uint64_t)max_ctas);
     if (k.layout == 2) {
-      grid = (uint64_t)oo_grid(k);  // equal-cost slices, one per CTA
+      grid = max_ctas > 0 ? std::min<uint64_t>((uint64_t)oo_grid(k), grid) : (uint64_t)oo_grid(k);  // equal-cost slices
     } else if (k.layout == 1) {
       // group-specialised: G groups x spg chunk ranges (grid must be a multiple of G)
       const uint64_t G = (uint64_t)k.n_groups;

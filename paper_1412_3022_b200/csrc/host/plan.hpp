@@ -115,7 +115,7 @@ int precompile_kernel(const PlanSpec &p, const GenOptions &o, std::string &err);
 
 // Launch over `stripes` stripes of S-byte blocks.  ptrs/strides: n_slots entries.
 int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides, size_t S, size_t stripes,
-                  void *stream, std::string &err);
+                  void *stream, std::string &err, int max_ctas = 0);  // max_ctas: grid cap (0 = one wave)
 
 std::atomic<unsigned long long> &launch_counter();
 

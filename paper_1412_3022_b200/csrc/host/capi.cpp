@@ -238,6 +238,7 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "own_first") c->gen.own_first = v != 0;
         if (key == "debug") c->gen.debug = v;
         if (key == "l2_shared") c->gen.l2_shared = v;
+        if (key == "ws") c->gen.ws = v != 0;
         if (key == "grid_ctas" && v > 0) c->gen.grid_ctas = v;
       }
       pos = e + 1;

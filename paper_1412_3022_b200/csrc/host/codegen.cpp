@@ -90,6 +90,7 @@ static __device__ __forceinline__ void pm_cp_commit() { asm volatile("cp.async.c
 static __device__ __forceinline__ void pm_cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 template <int N> static __device__ __forceinline__ void pm_cp_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 static __device__ __forceinline__ void pm_team_sync(u32 id, u32 n) { asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory"); }
+static __device__ __forceinline__ void pm_team_arrive(u32 id, u32 n) { asm volatile("bar.arrive %0, %1;" :: "r"(id), "r"(n) : "memory"); }
 static __device__ __forceinline__ void pm_bar_init(u32 bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar) : "memory");
 }
@@ -589,9 +590,13 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
 
   const int M = std::max(1, o.chunk_loop);
   // stage-buffer ring per team: NB buffers, prefetch distance D = NB - 1 stages (layouts 1/2)
-  const int NB = o.layout == 0 ? 2 : std::max(2, o.nbuf);
+  const int NB = (o.layout == 0 || (o.ws && o.team >= 2)) ? 2 : std::max(2, o.nbuf);
   const int D = NB - 1;
   const int T = std::max(1, o.team);  // warps sharing one chunk's stage buffer
+  // warp-specialised teams (o.ws, layouts 1/2): rank 0 loads and transposes every block of a
+  // stage (producer), ranks 1..T-1 run the XOR networks (consumers); named barriers FULL/EMPTY per
+  // stage buffer replace the team barrier (4 ids per team: teams <= 4, two buffers)
+  const bool WS = o.ws && o.layout >= 1 && T >= 2;
   std::ostringstream s;
   s << "// generated by libpmrc (codegen.cpp) — bitsliced GF(2^8) region linear combination\n";
   s << kHeader;
@@ -658,8 +663,8 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     o2 << ind << "  const u32 z0 = (okq && qo < S) ? 16u : 0u, z1 = (okq && qo + 512u < S) ? 16u : 0u;\n";
     o2 << ind << "  const u32 dst = sbuf + (" << bb << ") * (PM_QMAX * 1024u) + lane * 16u;\n";
     o2 << ind << "  switch (rank) {\n";
-    for (int rk = 0; rk < T; rk++) {
-      const int lo = n * rk / T, hi = n * (rk + 1) / T;
+    for (int rk = 0; rk < (WS ? 1 : T); rk++) {
+      const int lo = WS ? 0 : n * rk / T, hi = WS ? n : n * (rk + 1) / T;
       o2 << ind << "  case " << rk << ": {\n";
       std::map<int, bool> slots;
       for (int i = lo; i < hi; i++) slots[sg.blocks[i].first] = true;
@@ -723,7 +728,8 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     const int mall = (int)G.rows.size();
     s << "      switch (rank) {\n";
     for (int rk = 0; rk < T; rk++) {
-      const int r0 = mall * rk / T, r1 = mall * (rk + 1) / T;
+      const int r0 = WS ? (rk == 0 ? 0 : mall * (rk - 1) / (T - 1)) : mall * rk / T;
+      const int r1 = WS ? (rk == 0 ? 0 : mall * rk / (T - 1)) : mall * (rk + 1) / T;
       const int m = r1 - r0;
       s << "      case " << rk << ": {\n";
       std::vector<std::string> outs;
@@ -742,15 +748,33 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         const Stage &sg = stages[si];
         const int nblk = (int)sg.blocks.size();
         s << "        {\n";
+        if (WS) {
+          s << "          const u32 buf = sbuf + pb * (PM_QMAX * 1024u);\n";
+          if (rk == 0) {
+            // producer: data landed -> transpose every block -> FULL; wait until the consumers
+            // released the other buffer (EMPTY) before loading the successor stage into it
+            s << "          pm_cp_wait<0>();\n";
+            if (!(o.debug & 1)) s << "          pm_transpose_in(buf + lane * 16u, 0u, " << nblk << "u);\n";
+            s << "          pm_team_arrive(4u * team + pb, PM_T * 32u);\n";
+            s << "          if (kk != 0u" << (sj ? " || true" : "") << ") pm_team_sync(4u * team + 2u + (pb ^ 1u), PM_T * 32u);\n";
+            prefetch(g, sj);
+            s << "          pm_cp_commit();\n";
+          } else {
+            s << "          pm_team_sync(4u * team + pb, PM_T * 32u);\n";
+            s << "          const u32 pl = buf + lane * 16u;\n";
+          }
+        } else {
         // consume: own copies landed -> transpose own share -> team barrier
         s << "          pm_cp_wait<" << (D - 1) << ">();\n";
         s << "          const u32 buf = sbuf + pb * (PM_QMAX * 1024u);\n";
         if (!(o.debug & 1))  // debug bit 0: skip the input transposes (timing experiments only: wrong results)
           s << "          pm_transpose_in(buf + lane * 16u, " << nblk * rk / T << "u, " << nblk * (rk + 1) / T << "u);\n";
         s << "          const u32 pl = buf + lane * 16u;\n";
+        }
         // the team barrier + the prefetch of the successor stage into the other buffer; emitted
         // after the sub-networks that read only this warp's own transposed blocks (below)
         auto emit_sync = [&]() {
+          if (WS) return;  // producer / consumer barriers instead
           s << "          " << (T > 1 ? "pm_team_sync(1u + team, PM_T * 32u);" : "__syncwarp();") << "\n";
           prefetch(g, sj);
           s << "          pm_cp_commit();\n";
@@ -830,7 +854,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
           const int own_lo = nblk * rk / T, own_hi = nblk * (rk + 1) / T;
           std::vector<int> order_pre, order_post;
           for (size_t si2 = 0; si2 < subs.size(); si2++) {
-            bool own = T > 1 && o.own_first;
+            bool own = T > 1 && o.own_first && !WS;
             const int cc0 = (int)si2 * sub, cc1 = std::min(ncols, cc0 + sub);
             for (int ci = cc0; ci < cc1 && own; ci++) {
               const InputDesc &in = p.inputs[sg.cols[ci]];
@@ -888,6 +912,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
           for (int si2 : order_post) emit_sub(si2);
           first = false;
         }
+        if (WS && rk > 0) s << "          pm_team_arrive(4u * team + 2u + pb, PM_T * 32u);\n";
         s << (NB == 2 ? "          pb ^= 1u;\n" : "          pb = pb + 1u == " + std::to_string(NB) + "u ? 0u : pb + 1u;\n");
         s << "        }\n";
         if (rk == 0) {
@@ -1072,6 +1097,8 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
       s << "        }\n      }\n";
     }
     s << "    }\n";
+    if (WS)  // balance the last EMPTY arrival of the consumers (the producer's final wait)
+      s << "    if (rank == 0u && c0 + team < c1) pm_team_sync(4u * team + 2u + (pb ^ 1u), PM_T * 32u);\n";
     s << "  } break;\n";
   }
   s << "  default: break;\n  }\n";

@@ -239,6 +239,7 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "debug") c->gen.debug = v;
         if (key == "l2_shared") c->gen.l2_shared = v;
         if (key == "ws") c->gen.ws = v != 0;
+        if (key == "ws_prod" && v > 0) c->gen.ws_prod = v;
         if (key == "grid_ctas" && v > 0) c->gen.grid_ctas = v;
       }
       pos = e + 1;

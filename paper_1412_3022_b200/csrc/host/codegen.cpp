@@ -597,6 +597,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   // stage (producer), ranks 1..T-1 run the XOR networks (consumers); named barriers FULL/EMPTY per
   // stage buffer replace the team barrier (4 ids per team: teams <= 4, two buffers)
   const bool WS = o.ws && o.layout >= 1 && T >= 2;
+  const int NP = WS ? std::max(1, std::min(T - 1, o.ws_prod)) : 0;  // producer warps per team
   std::ostringstream s;
   s << "// generated by libpmrc (codegen.cpp) — bitsliced GF(2^8) region linear combination\n";
   s << kHeader;
@@ -663,8 +664,8 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     o2 << ind << "  const u32 z0 = (okq && qo < S) ? 16u : 0u, z1 = (okq && qo + 512u < S) ? 16u : 0u;\n";
     o2 << ind << "  const u32 dst = sbuf + (" << bb << ") * (PM_QMAX * 1024u) + lane * 16u;\n";
     o2 << ind << "  switch (rank) {\n";
-    for (int rk = 0; rk < (WS ? 1 : T); rk++) {
-      const int lo = WS ? 0 : n * rk / T, hi = WS ? n : n * (rk + 1) / T;
+    for (int rk = 0; rk < (WS ? NP : T); rk++) {
+      const int lo = WS ? n * rk / NP : n * rk / T, hi = WS ? n * (rk + 1) / NP : n * (rk + 1) / T;
       o2 << ind << "  case " << rk << ": {\n";
       std::map<int, bool> slots;
       for (int i = lo; i < hi; i++) slots[sg.blocks[i].first] = true;
@@ -728,8 +729,8 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     const int mall = (int)G.rows.size();
     s << "      switch (rank) {\n";
     for (int rk = 0; rk < T; rk++) {
-      const int r0 = WS ? (rk == 0 ? 0 : mall * (rk - 1) / (T - 1)) : mall * rk / T;
-      const int r1 = WS ? (rk == 0 ? 0 : mall * rk / (T - 1)) : mall * (rk + 1) / T;
+      const int r0 = WS ? (rk < NP ? 0 : mall * (rk - NP) / (T - NP)) : mall * rk / T;
+      const int r1 = WS ? (rk < NP ? 0 : mall * (rk - NP + 1) / (T - NP)) : mall * (rk + 1) / T;
       const int m = r1 - r0;
       s << "      case " << rk << ": {\n";
       std::vector<std::string> outs;
@@ -750,11 +751,12 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         s << "        {\n";
         if (WS) {
           s << "          const u32 buf = sbuf + pb * (PM_QMAX * 1024u);\n";
-          if (rk == 0) {
-            // producer: data landed -> transpose every block -> FULL; wait until the consumers
-            // released the other buffer (EMPTY) before loading the successor stage into it
+          if (rk < NP) {
+            // producer: data landed -> transpose its share of the blocks -> FULL; wait until the
+            // consumers released the other buffer (EMPTY) before loading the successor stage
             s << "          pm_cp_wait<0>();\n";
-            if (!(o.debug & 1)) s << "          pm_transpose_in(buf + lane * 16u, 0u, " << nblk << "u);\n";
+            if (!(o.debug & 1))
+              s << "          pm_transpose_in(buf + lane * 16u, " << nblk * rk / NP << "u, " << nblk * (rk + 1) / NP << "u);\n";
             s << "          pm_team_arrive(4u * team + pb, PM_T * 32u);\n";
             s << "          if (kk != 0u" << (sj ? " || true" : "") << ") pm_team_sync(4u * team + 2u + (pb ^ 1u), PM_T * 32u);\n";
             prefetch(g, sj);
@@ -912,7 +914,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
           for (int si2 : order_post) emit_sub(si2);
           first = false;
         }
-        if (WS && rk > 0) s << "          pm_team_arrive(4u * team + 2u + pb, PM_T * 32u);\n";
+        if (WS && rk >= NP) s << "          pm_team_arrive(4u * team + 2u + pb, PM_T * 32u);\n";
         s << (NB == 2 ? "          pb ^= 1u;\n" : "          pb = pb + 1u == " + std::to_string(NB) + "u ? 0u : pb + 1u;\n");
         s << "        }\n";
         if (rk == 0) {
@@ -1098,7 +1100,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     }
     s << "    }\n";
     if (WS)  // balance the last EMPTY arrival of the consumers (the producer's final wait)
-      s << "    if (rank == 0u && c0 + team < c1) pm_team_sync(4u * team + 2u + (pb ^ 1u), PM_T * 32u);\n";
+      s << "    if (rank < " << NP << "u && c0 + team < c1) pm_team_sync(4u * team + 2u + (pb ^ 1u), PM_T * 32u);\n";
     s << "  } break;\n";
   }
   s << "  default: break;\n  }\n";

@@ -84,9 +84,9 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     oo.layout = (G <= sms && (sms % G) * 10 <= sms) ? 1 : 0;
     if (oo.layout == 1 && g0.group_cost_ratio > 1.2) oo.layout = 2;  // unequal groups: apportion CTAs
   }
-  if (oo.ws) {  // producer + 2 consumers per team, 4 teams (4 named barriers per team), 2 buffers
-    oo.team = 3;
-    oo.warps = 12;
+  if (oo.ws) {  // ws_prod producers + 2 consumers per team, <= 4 teams (4 named barriers each), 2 buffers
+    oo.team = std::max(1, oo.ws_prod) + 2;
+    oo.warps = oo.team * std::min(4, 12 / oo.team);
     oo.nbuf = 2;
   }
   // warps per CTA from the shared-memory budget (2 stage buffers of in_block KiB per team)

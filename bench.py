@@ -151,6 +151,7 @@ def main():
     import inputs
     import paper_1412_3022_b200 as pm
     from paper_1412_3022_b200 import build as pmbuild
+    from paper_1412_3022_b200 import dist as pdist
     pmbuild.build_all(kernels=False)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -198,12 +199,11 @@ def main():
     barrier()
     per = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[-1])
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    # max over ranks of the device-timed region, whole-job throughput (paper_1412_3022_b200/dist.py,
+    # covered by the gloo world_size-2 test)
+    total_ms = pdist.max_over_ranks(total_ms, dist if world > 1 else None, device=dev)
     ms_step = total_ms / args.steps
-    value = world * REAL / (ms_step * 1e-3) / 1e9
+    value = pdist.aggregate_gbps(REAL, world, ms_step * 1e-3)
 
     # ---- roofline of the (only) kernel: pmrc_kernel, one launch per step ----
     pk = peaks()
@@ -249,10 +249,8 @@ def main():
             t0 = time.perf_counter()
             pm.pmrc_encode_host(code, hd.data_ptr(), hp.data_ptr(), S_, stripes, stream.cuda_stream)
             times.append(time.perf_counter() - t0)
-        tt = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * REAL / float(tt.item()) / 1e9, "unit": "GB/s",
+        tmax = pdist.max_over_ranks(sum(times) / len(times), dist if world > 1 else None, device=dev)
+        e2e = {"value": pdist.aggregate_gbps(REAL, world, tmax), "unit": "GB/s",
                "h2d_bytes_per_step": stripes * B * S_, "d2h_bytes_per_step": stripes * P * S_,
                "api": "pmrc_encode_host (pinned host buffers, staged + overlapped copies)"}
         del hd, hp

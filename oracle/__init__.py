@@ -272,6 +272,17 @@ def repair_project(kind, n, k, d, f, piece):
     return beta
 
 
+def repair_combine(kind, n, k, d, f, H, betas):
+    """Newcomer side: betas (len(H), S) of helpers H -> lost piece (alpha, S)."""
+    H = _i32(H)
+    betas = _u8(betas)
+    alpha, B = params(kind, n, k, d)
+    S = betas.shape[1]
+    out = np.zeros((alpha, S), np.uint8)
+    _chk(_lib().or_repair_combine(kind, n, k, d, f, _p(H), _p(betas), _p(out), S), "repair_combine")
+    return out
+
+
 def repair(kind, n, k, d, f, H, pieces):
     """H: helper ids (d of them; RS: k); pieces (len(H), alpha, S) -> lost piece (alpha, S).
     Raises OracleError(rc=ESING) if Psi_H is singular."""

@@ -35,3 +35,45 @@ def max_over_ranks(value, dist=None, device=None):
 def aggregate_gbps(bytes_per_rank, world, max_seconds):
     """Whole-job throughput: all ranks' bytes over the slowest rank's time."""
     return world * bytes_per_rank / max_seconds / 1e9
+
+
+def distributed_repair(lost_id, helper_ids, owner, pieces, newcomer_out, project, combine, beta_like, dist=None,
+                       rank=0):
+    """Exact repair with the helpers and the newcomer on different ranks (the
+    network step the codes exist to minimise, P:42, P:53 footnote): every rank projects the pieces
+    of the helpers it owns onto phi_f / psi_f (``project(h, piece) -> beta``, the product's
+    pmrc_repair_project on GPUs), ships each beta -- one block per stripe, d blocks in all instead
+    of k*alpha for a decode-based repair -- to the newcomer's rank (point-to-point send/recv: NCCL
+    over NVLink on GPUs, gloo in the CPU tests), and the newcomer's rank combines them
+    (``combine(helper_ids, betas) -> piece``, pmrc_repair_combine).
+
+    owner: node id -> rank; pieces: {node id: piece} for the helpers this rank owns;
+    beta_like: an empty tensor of the beta shape/dtype/device (receive buffers);
+    newcomer_out: the caller's output (written on the newcomer's rank only, via combine).
+    Returns the number of bytes this rank sent to another rank."""
+    new_rank = owner[lost_id]
+    betas = {}
+    sent = 0
+    reqs = []
+    for h in helper_ids:
+        if owner[h] != rank:
+            continue
+        b = project(h, pieces[h])
+        if rank == new_rank:
+            betas[h] = b
+        else:
+            reqs.append(dist.isend(b, dst=new_rank))   # per (src, dst) pair in helper order
+            sent += b.numel() * b.element_size()
+    if rank == new_rank:
+        recv = {}
+        for h in helper_ids:
+            if owner[h] != rank:
+                buf = beta_like.clone()
+                recv[h] = (buf, dist.irecv(buf, src=owner[h]))
+        for h, (buf, rq) in recv.items():
+            rq.wait()
+            betas[h] = buf
+        combine(helper_ids, [betas[h] for h in helper_ids], newcomer_out)
+    for rq in reqs:
+        rq.wait()
+    return sent

@@ -76,3 +76,59 @@ def test_two_rank_gloo_sharded_encode_and_max_time():
     got = np.concatenate([np.frombuffer(r[3], np.uint8).reshape(r[2] - r[1], 6, 64) for r in res])
     assert np.array_equal(got, full)          # the ranks' stripes tile the job exactly
     assert all(r[4] == 1.25 for r in res)     # max over ranks, seen by every rank
+
+
+def _repair_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    import inputs
+    import oracle as O
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # MSR k=4 n=8 (d=6): nodes spread over the ranks, the lost node's newcomer on owner[f]
+    kind, k, n, d, S = O.MSR_SPARSE, 4, 8, 6, 96
+    alpha, B = O.params(kind, n, k, d)
+    code = O.full_code(kind, n, k, d, inputs.stripe_data(1, B, S, seed=13)[0])   # (n, alpha, S)
+    owner = {i: i % world for i in range(n)}
+    res = []
+    for f, H in ((5, [0, 1, 2, 3, 4, 6]), (1, [0, 2, 3, 5, 6, 7])):
+        pieces = {h: torch.from_numpy(code[h].copy()) for h in H if owner[h] == rank}
+        out = torch.zeros((alpha, S), dtype=torch.uint8)
+
+        def project(h, piece):
+            return torch.from_numpy(O.repair_project(kind, n, k, d, f, piece.numpy()))
+
+        def combine(ids, betas, dst):
+            dst.copy_(torch.from_numpy(O.repair_combine(kind, n, k, d, f, ids, torch.stack(betas).numpy())))
+        sent = pdist.distributed_repair(f, H, owner, pieces, out, project, combine,
+                                        torch.empty(S, dtype=torch.uint8), dist, rank)
+        res.append((f, sent, out.numpy().tobytes() if owner[f] == rank else None,
+                    code[f].tobytes()))
+    q.put((rank, res))
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_distributed_repair():
+    # NEXT-3: helpers project locally, ship one block each to the newcomer's rank, which combines;
+    # the regenerated piece is exact and each rank sends exactly its remote helpers' betas
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_repair_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    S = 96
+    for idx, (f, H) in enumerate(((5, [0, 1, 2, 3, 4, 6]), (1, [0, 2, 3, 5, 6, 7]))):
+        new_rank = f % world
+        got = res[new_rank][idx][2]
+        assert got == res[new_rank][idx][3]                      # exact regeneration
+        for r in range(world):
+            remote = sum(1 for h in H if h % world == r and r != new_rank)
+            assert res[r][idx][1] == remote * S                   # d blocks in total, one per helper

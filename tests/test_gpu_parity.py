@@ -459,3 +459,32 @@ def test_decode_and_repair_write_only_their_outputs():
         assert torch.equal(big[: stripes * st.alpha * S].view(stripes, st.alpha, S), st.piece_tensor(f))
     finally:
         st.close()
+
+
+def test_distributed_repair_single_rank_with_product_kernels():
+    # NEXT-3's orchestration (paper_1412_3022_b200/dist.py) with the product's projection and
+    # combine kernels; all helpers on this rank (the gloo test covers the cross-rank transfers)
+    from paper_1412_3022_b200 import dist as pdist
+    k, n, S, stripes = 8, 16, 2048 + 16, 2
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=95)
+    try:
+        st.encode()
+        f, H = 11, [i for i in range(n) if i not in (11, 14)]
+        owner = {i: 0 for i in range(n)}
+
+        def project(h, piece):
+            b = torch.empty((stripes, S), dtype=torch.uint8, device=DEV)
+            pm.pmrc_repair_project(st.code, f, piece, (b.data_ptr(), S), S, stripes, st.stream)
+            return b
+
+        def combine(ids, betas, dst):
+            pm.pmrc_repair_combine(st.code, f, ids, [(b.data_ptr(), S) for b in betas],
+                                   (dst.data_ptr(), st.alpha * S), S, stripes, st.stream)
+        out = torch.empty((stripes, st.alpha, S), dtype=torch.uint8, device=DEV)
+        sent = pdist.distributed_repair(f, H, owner, {h: st.piece(h) for h in H}, out, project, combine,
+                                        torch.empty((stripes, S), dtype=torch.uint8, device=DEV), None, 0)
+        torch.cuda.synchronize()
+        assert sent == 0
+        assert torch.equal(out, st.piece_tensor(f))
+    finally:
+        st.close()

@@ -835,7 +835,12 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
           // within a sub-network only): temps and plane quads then die at sub-network boundaries,
           // which bounds register pressure for wide plans (decode) at the price of some sharing
           const int ncols = (int)sg.cols.size();
-          const int sub = o.net_in > 0 ? o.net_in : ncols;
+          // equal-sized sub-networks of at most net_in inputs (14 -> 7 + 7, 8 -> 4 + 4, not 7 + 1)
+          int sub = o.net_in > 0 ? o.net_in : ncols;
+          if (o.net_even && sub < ncols) {
+            const int nsub = (ncols + sub - 1) / sub;
+            sub = (ncols + nsub - 1) / nsub;
+          }
           std::vector<Slp> subs;
           std::vector<std::vector<std::string>> sub_base;
           for (int c0 = 0; c0 < ncols; c0 += sub) {

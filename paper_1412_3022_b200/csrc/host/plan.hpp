@@ -62,6 +62,7 @@ struct GenOptions {
   int nbuf = 2;             // stage buffers per team (layouts 1/2): prefetch nbuf-1 stages ahead
   int tr_unroll = 1;        // unroll factor of the in-place input transpose loop
   bool fence = true;        // register fence after every (sub-)network (see codegen.cpp)
+  bool net_even = true;     // split a stage into equal sub-networks (<= net_in inputs each)
   int net_in = 7;           // inputs per CSE sub-network within a stage (0 = the whole stage)
   bool trace = false;       // layout 1 diagnostics: per-team start/end/wait times (pmrc_debug_counters)
   int pace_lag = 0;         // layout 1: max chunks a team runs ahead of its peers (0 = no pacing)

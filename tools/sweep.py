@@ -117,12 +117,13 @@ def emit(d):
     print(json.dumps(d), flush=True)
 
 
-def run_encode(kind, k, n, S, steps):
-    j = Job(kind, k, n, S)
+def run_encode(kind, k, n, S, steps, real=1 << 30):
+    j = Job(kind, k, n, S, real=real)
     ms = timed(j.encode, steps)
     src = j.stripes * j.B * j.S
     emit({"op": "encode", "kind": KIND_NAMES[kind], "k": k, "n": n, "S": S,
-          "stripes": j.stripes, "ms": round(ms, 4), "GBps": round(src / ms / 1e6, 1), "init_s": round(j.init_s, 2),
+          "stripes": j.stripes, "source_bytes": real, "ms": round(ms, 4), "GBps": round(src / ms / 1e6, 1),
+          "init_s": round(j.init_s, 2),
           "roofline": roofline(j.code, 2, 0, [], S, j.stripes, ms)})
     return j
 
@@ -282,6 +283,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--sizes", default="4,16,64,256,1024,4096", help="config-5 sub-block sizes (KiB)")
     ap.add_argument("--ks", default="4,8,16")
+    ap.add_argument("--gib", type=float, default=8.0, help="config-5 source GiB per GPU (64 GiB / 8 GPUs)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     rng = inputs.rng(2026)
@@ -343,12 +345,15 @@ def main():
                       "bit_exact": ok if name == "precode_then_encode" else None})
             j.close()
     if "5" in cfgs:
+        # BASELINE.json config 5: 64 GiB per point over 8 GPUs = args.gib (8) GiB per GPU; this
+        # process is one of those GPUs (weak scaling, no data-path collective)
+        real = int(args.gib * (1 << 30))
         for kind in (MSR, MBR):
             for k in [int(x) for x in args.ks.split(",")]:
                 for kib in [int(x) for x in args.sizes.split(",")]:
-                    run_encode(kind, k, 2 * k, kib << 10, args.steps).close()
+                    run_encode(kind, k, 2 * k, kib << 10, args.steps, real).close()
         for kib in [int(x) for x in args.sizes.split(",")]:
-            run_encode(RS, 8, 16, kib << 10, args.steps).close()
+            run_encode(RS, 8, 16, kib << 10, args.steps, real).close()
 
 
 if __name__ == "__main__":

@@ -230,6 +230,7 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "trace") c->gen.trace = v != 0;
         if (key == "net_in") c->gen.net_in = v;
         if (key == "net_even") c->gen.net_even = v != 0;
+        if (key == "stage_even") c->gen.stage_even = v != 0;
         if (key == "fence") c->gen.fence = v != 0;
         if (key == "tr_unroll" && v > 0) c->gen.tr_unroll = v;
         if (key == "sched") c->gen.sched = v != 0;

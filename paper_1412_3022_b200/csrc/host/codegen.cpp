@@ -539,10 +539,18 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   for (size_t g = 0; g < groups.size(); g++) {
     Stage cur;
     cur.g = (int)g;
+    // balanced stages: as few as IB allows, of equal size (30 inputs -> 15 + 15, not 14 + 14 + 2)
+    int cap = IB;
+    if (o.stage_even) {
+      int tot = 0;
+      for (int c : groups[g].cols) tot += (int)p.inputs[c].terms.size();
+      const int nst = std::max(1, (tot + IB - 1) / IB);
+      cap = std::min(IB, (tot + nst - 1) / nst);
+    }
     for (int c : groups[g].cols) {
       const InputDesc &in = p.inputs[c];
       int need = (int)in.terms.size();
-      if (!cur.cols.empty() && (int)cur.blocks.size() + need > IB) {
+      if (!cur.cols.empty() && (int)cur.blocks.size() + need > cap) {
         gstages[g].push_back((int)stages.size());
         stages.push_back(cur);
         cur = Stage();

@@ -66,11 +66,6 @@ static __device__ __forceinline__ uint4 pm_lds(u32 a) {
 static __device__ __forceinline__ void pm_sts(u32 a, u32 x, u32 y, u32 z, u32 w) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
-static __device__ __forceinline__ u64 pm_lds64(u32 a) {
-  u64 v;
-  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
-  return v;
-}
 // 16-B async copy global -> shared with an L2 cache policy; src_size 0 zero-fills (no branch)
 static __device__ __forceinline__ void pm_cp16(u32 dst, const void *src, u32 src_size, u64 pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;"
@@ -87,23 +82,9 @@ static __device__ __forceinline__ u64 pm_policy_en() {
   return p;
 }
 static __device__ __forceinline__ void pm_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-static __device__ __forceinline__ void pm_cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 template <int N> static __device__ __forceinline__ void pm_cp_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 static __device__ __forceinline__ void pm_team_sync(u32 id, u32 n) { asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory"); }
 static __device__ __forceinline__ void pm_team_arrive(u32 id, u32 n) { asm volatile("bar.arrive %0, %1;" :: "r"(id), "r"(n) : "memory"); }
-static __device__ __forceinline__ void pm_bar_init(u32 bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar) : "memory");
-}
-static __device__ __forceinline__ void pm_bar_expect(u32 bar, u32 bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
-}
-static __device__ __forceinline__ void pm_bar_wait(u32 bar, u32 parity) {
-  u32 ok;
-  do {
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
-  } while (!ok);
-}
 // pacing of group-specialised CTAs (layout 1): wait until the n peer counters p[i * stride] reach
 // `want`; bounded (a peer that is not resident must never deadlock us): after a timeout the caller
 // stops pacing for the rest of the launch.  Counters are (epoch << 32 | chunks done).
@@ -138,14 +119,6 @@ static __device__ __forceinline__ u64 pm_gtime() {
 }
 static __device__ __forceinline__ void pm_pace_post(u64 *p, u64 v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
-}
-static __device__ __forceinline__ void pm_bulk(u32 dst, const void *src, u32 bytes, u32 bar, bool ef, u64 pol) {
-  if (ef)
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-                 :: "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
-  else
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 )CUDA";
 

@@ -246,6 +246,40 @@ def pmrc_plan_stats(code, op, lost_id=0, ids=()):
     return {f: getattr(st, f) for f, _ in pmrc_plan_stats_t._fields_}
 
 
+def prepare_plans(kind, k, d, n, patterns, threads=None):
+    """Pre-compile the decode / repair plans of many failure patterns in parallel (NVRTC runs
+    outside the GIL; each worker thread uses its own handle, and the cubins land in the shared
+    in-tree kernel cache, keyed by source), so that the first pmrc_decode / pmrc_repair of each
+    pattern only loads a cubin.  patterns: iterable of ("decode", survivor_ids) or
+    ("repair", lost_id, helper_ids).  Returns the list of (pattern, rc) (rc = PMRC_ESINGULAR for
+    singular helper sets)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    pats = list(patterns)
+    threads = threads or min(len(pats), os.cpu_count() or 4) or 1
+    handles = [pmrc_create(kind, k, d, n) for _ in range(threads)]
+    try:
+        def work(i):
+            h = handles[i % threads]
+            out = []
+            for pt in pats[i::threads]:
+                try:
+                    if pt[0] == "decode":
+                        pmrc_plan_source(h, 0, 0, pt[1], compile=True)
+                    else:
+                        pmrc_plan_source(h, 1, pt[1], pt[2], compile=True)
+                    out.append((pt, PMRC_OK))
+                except PmrcError as e:
+                    out.append((pt, e.rc))
+            return out
+        with ThreadPoolExecutor(threads) as ex:
+            res = [r for part in ex.map(work, range(threads)) for r in part]
+    finally:
+        for h in handles:
+            pmrc_destroy(h)
+    return res
+
+
 def pmrc_debug_counters(code):
     """Pacing counters / trace of the encode kernel as a list of ints (diagnostics)."""
     n = ctypes.c_size_t(0)

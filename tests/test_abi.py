@@ -131,3 +131,19 @@ def test_plan_stats_and_source_without_gpu():
         assert "pmrc_kernel" in src and "lop3" in src
     finally:
         pm.pmrc_destroy(c)
+
+
+def test_prepare_plans_parallel_without_gpu():
+    # config-4-style patterns compiled in parallel host threads (no GPU): singular helper sets (R10)
+    # and all-systematic survivor sets are reported, the rest compile
+    pats = [("repair", 15, [i for i in range(16) if i not in (15, 3)]),
+            ("repair", 0, [i for i in range(16) if i not in (0, 1)]),        # R10 singular
+            ("decode", [0, 1, 2, 3, 12, 13, 14, 15]),
+            ("decode", list(range(8)))]                                      # nothing to decode
+    res = dict((str(p), rc) for p, rc in pm.prepare_plans(pm.PMRC_MSR_SPARSE, 3, 4, 6, []))
+    assert res == {}
+    out = pm.prepare_plans(pm.PMRC_MSR_SPARSE, 8, 14, 16, pats, threads=2)
+    rcs = {str(p): rc for p, rc in out}
+    assert rcs[str(pats[0])] == pm.PMRC_OK and rcs[str(pats[2])] == pm.PMRC_OK
+    assert rcs[str(pats[1])] == pm.PMRC_ESINGULAR
+    assert rcs[str(pats[3])] == pm.PMRC_EINVAL

@@ -62,6 +62,8 @@ def _lib():
             "or_repair_mu": ([I, I, I, I, I, P, P], I),
             "or_repair_reads": ([I, I, I, I, I], I),
             "or_repair_project": ([I, I, I, I, I, P, P, Z], I),
+            "or_validate16_sparse": ([I, ctypes.POINTER(ctypes.c_int)], I),
+            "or_gf16_mul": ([ctypes.c_uint16, ctypes.c_uint16], ctypes.c_uint16),
             "or_repair_combine": ([I, I, I, I, I, P, P, P, Z], I),
             "or_repair": ([I, I, I, I, I, P, P, P, Z], I),
             "or_validate": ([I, I, I, I, ctypes.c_long, I, P], I),
@@ -270,6 +272,19 @@ def repair_project(kind, n, k, d, f, piece):
     beta = np.zeros(S, np.uint8)
     _chk(_lib().or_repair_project(kind, n, k, d, f, _p(piece), _p(beta), S), "repair_project")
     return beta
+
+
+def gf16_mul(a, b):
+    """GF(2^16) product, polynomial 0x1100B (R1 extended to w = 16)."""
+    return int(_lib().or_gf16_mul(a, b))
+
+
+def validate16_sparse(k):
+    """P:189 in GF(2^16): flags of the sparse construction at n = d+1 (1 lambda collision,
+    2 a singular d x d submatrix of Psi)."""
+    f = ctypes.c_int(0)
+    _chk(_lib().or_validate16_sparse(k, ctypes.byref(f)), "validate16_sparse")
+    return f.value
 
 
 def repair_combine(kind, n, k, d, f, H, betas):

@@ -852,3 +852,83 @@ int or_validate(int kind, int n, int k, int d, long max_subsets, int check_phi, 
   free(lam);
   return flags;
 }
+
+/* ------------------------------------------------------------------ GF(2^16) validity */
+/* P:189's second claim: the sparse construction is valid for k in {2..64} in GF(2^16).  Reading
+ * R1 extended to w = 16 (GF-Complete's default, as for w = 8): primitive polynomial
+ * x^16+x^12+x^3+x+1 (0x1100B), g = 2.  The sparse Psi (same formulas and 1-based indices as
+ * or_psi) at n = d+1, checked like P:189 describes: Lambda distinct, and all n d x d submatrices
+ * of Psi invertible.  Returns flags as or_validate (1 lambda collision, 2 singular submatrix). */
+static uint16_t EXP16[2 * 65535];
+static int LOG16[65536];
+static int gf16_ready = 0;
+static void gf16_init(void) {
+  if (gf16_ready) return;
+  unsigned x = 1;
+  for (int e = 0; e < 65535; e++) {
+    EXP16[e] = (uint16_t)x;
+    LOG16[x] = e;
+    x <<= 1;
+    if (x & 0x10000) x ^= 0x1100B;
+  }
+  for (int e = 65535; e < 2 * 65535; e++) EXP16[e] = EXP16[e - 65535];
+  LOG16[0] = -1;
+  gf16_ready = 1;
+}
+static uint16_t gf16_mul(uint16_t a, uint16_t b) {
+  if (!a || !b) return 0;
+  return EXP16[LOG16[a] + LOG16[b]];
+}
+static uint16_t gf16_inv(uint16_t a) { return EXP16[(65535 - LOG16[a]) % 65535]; }
+static uint16_t gf16_exp(long e) { return EXP16[((e % 65535) + 65535) % 65535]; }
+static int gf16_rank(uint16_t *W, int r, int c) {
+  int rank = 0;
+  for (int col = 0; col < c && rank < r; col++) {
+    int piv = -1;
+    for (int i = rank; i < r; i++)
+      if (W[i * c + col]) { piv = i; break; }
+    if (piv < 0) continue;
+    if (piv != rank)
+      for (int j = 0; j < c; j++) { uint16_t t = W[piv * c + j]; W[piv * c + j] = W[rank * c + j]; W[rank * c + j] = t; }
+    uint16_t inv = gf16_inv(W[rank * c + col]);
+    for (int i = 0; i < r; i++) {
+      if (i == rank || !W[i * c + col]) continue;
+      uint16_t f = gf16_mul(W[i * c + col], inv);
+      for (int j = 0; j < c; j++) W[i * c + j] ^= gf16_mul(f, W[rank * c + j]);
+    }
+    rank++;
+  }
+  return rank;
+}
+uint16_t or_gf16_mul(uint16_t a, uint16_t b) { gf16_init(); return gf16_mul(a, b); }
+
+int or_validate16_sparse(int k, int *flags_out) {
+  gf16_init();
+  if (k < 2 || k > 200) return OR_EINVAL;
+  const int alpha = k - 1, d = 2 * k - 2, n = d + 1;
+  uint16_t *psi = (uint16_t *)malloc(sizeof(uint16_t) * n * d), *lam = (uint16_t *)malloc(sizeof(uint16_t) * n);
+  uint16_t *M = (uint16_t *)malloc(sizeof(uint16_t) * d * d);
+  for (int i = 1; i <= n; i++) {
+    uint16_t xi = gf16_exp(i + alpha);
+    uint16_t l = gf16_mul(xi ^ gf16_exp(0), gf16_inv(xi ^ gf16_exp(alpha)));
+    lam[i - 1] = l;
+    for (int j = 1; j <= alpha; j++) {
+      uint16_t phi = (i <= alpha) ? (uint16_t)(i == j) : gf16_inv(xi ^ gf16_exp(j - 1));
+      psi[(i - 1) * d + (j - 1)] = phi;
+      psi[(i - 1) * d + alpha + (j - 1)] = gf16_mul(l, phi);
+    }
+  }
+  int flags = 0;
+  for (int a = 0; a < n; a++)
+    for (int b = 0; b < a; b++)
+      if (lam[a] == lam[b]) flags |= 1;
+  for (int skip = 0; skip < n && !(flags & 2); skip++) { /* the n d-subsets: all rows but one */
+    int r = 0;
+    for (int i = 0; i < n; i++)
+      if (i != skip) memcpy(M + (size_t)(r++) * d, psi + (size_t)i * d, sizeof(uint16_t) * d);
+    if (gf16_rank(M, d, d) < d) flags |= 2;
+  }
+  free(psi); free(lam); free(M);
+  *flags_out = flags;
+  return OR_OK;
+}

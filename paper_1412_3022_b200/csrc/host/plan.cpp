@@ -94,10 +94,10 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
   (void)generate_source(p, oo, probe);
   int budget = 220 * 1024;
   int w = std::max(1, std::min(16, budget / std::max(1, probe.smem_per_warp)));
-  // measured (profiles/r01b): 12 warps for single-stage groups (encode); 8 for wide multi-stage
-  // groups (decode: 4 stages of 14 inputs), where fewer, larger-register warps schedule better
+  // 12 warps (6 teams of 2): measured best for encode, and for the multi-stage repair plans
+  // (config-4 repair 0.421 -> 0.404 ms vs 8 warps); wide decode plans set 16 above (auto_wide)
   int want = oo.warps;
-  if (want <= 0) want = probe.max_stages >= 3 ? 8 : 12;
+  if (want <= 0) want = 12;
   w = std::min(w, want);
   w = std::max(oo.team, w - w % std::max(1, oo.team));  // whole teams
   oo.warps = w;

@@ -40,7 +40,7 @@ struct GenOptions {
   int max_rows = 8;      // output blocks per group (8 planes each in registers)
   int in_block = 16;     // max loaded blocks per stage (shared-memory buffer of in_block KiB, x2)
   bool stage_even = true;  // split a group's inputs into equal stages of <= in_block blocks
-  int warps = 0;         // warps per CTA (0 = auto: 12, or 8 for plans of >= 3 stages per group; capped by smem)
+  int warps = 0;         // warps per CTA (0 = auto: 12; 16 for wide decode plans; capped by smem)
   int tpb = 256;         // (derived) threads per CTA
   bool cse = true;       // Paar CSE (false: naive per-row XOR chains)
   bool sync_groups = true;  // __syncthreads() before each group: warps of a CTA execute the same code

@@ -56,15 +56,17 @@ def build_inputs(force=False):
 # encode plans pre-compiled (NVRTC, sm_100a) into the in-tree kernel cache by build(): the bench
 # configuration and the GPU-test shapes.  (kind, k, d, n)
 PRECOMPILE = [(0, 8, 14, 16), (0, 3, 4, 6), (2, 8, 14, 16), (3, 8, 8, 16), (0, 8, 14, 15), (1, 8, 14, 16),
-              (0, 4, 6, 8), (2, 4, 6, 8), (0, 2, 2, 3), (1, 3, 4, 6), (2, 3, 4, 6), (3, 3, 3, 6), (0, 16, 30, 32), (2, 16, 30, 32)]
+              (0, 4, 6, 8), (2, 4, 6, 8), (0, 2, 2, 3), (1, 3, 4, 6), (2, 3, 4, 6), (3, 3, 3, 6), (0, 16, 30, 32), (2, 16, 30, 32),
+              (0, 8, 14, 16, 16), (0, 4, 6, 8, 16), (0, 8, 14, 15, 16)]   # + GF(2^16) encodes (w = 16)
 
 
 def _precompile_one(args):
     import ctypes
     L = ctypes.CDLL(LIB)
     h = ctypes.c_void_p()
-    kind, k, d, n = args
-    rc = L.pmrc_create(ctypes.byref(h), kind, k, d, n, 8)
+    kind, k, d, n = args[:4]
+    w = args[4] if len(args) > 4 else 8
+    rc = L.pmrc_create(ctypes.byref(h), kind, k, d, n, w)
     if rc == 0:
         rc = L.pmrc_precompile(h)
         L.pmrc_destroy(h)

@@ -48,6 +48,7 @@ struct pmrc_code {
   std::map<std::string, int> plan_err;                   // cached failures (ESINGULAR)
   std::map<std::string, int> plan_meta;                  // e.g. blocks written by a decode plan
   HostStage hs;
+  int w = 8;                   // symbol width (16: GF(2^16) encode only)
   int max_ctas = 0;            // pmrc_set_max_ctas: grid cap for every launch (0 = one full wave)
   std::string *dry = nullptr;  // pmrc_plan_source: get_kernel stores the generated source here instead
   PlanSpec dry_spec;           //   and the plan
@@ -247,14 +248,32 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
       pos = e + 1;
     }
   }
-  int rc = build_code(kind, k, d, n, w, c->def, err);
-  if (rc) return fail(rc, err);
+  int rc;
+  if (w == 16) {
+    // GF(2^16): sparse MSR encode only; the symbols are little-endian byte pairs
+    if (kind != KIND_MSR_SPARSE) return fail(PMRC_EUNSUPPORTED, "w = 16: only the sparse MSR code (kind 0)");
+    int alpha = 0, B = 0;
+    std::vector<uint16_t> gpp;
+    rc = build_gpp16(k, d, n, alpha, B, gpp, err);
+    if (rc) return fail(rc, err);
+    CodeDef &D = c->def;
+    D.kind = kind; D.n = n; D.k = k; D.d = d; D.alpha = alpha; D.B = B; D.P = (n - k) * alpha;
+    D.repair_complete = false;
+    c->w = 16;
+    c->enc_spec.w = 16;
+    c->enc_spec.A16 = gpp;
+    c->enc_spec.A = Mat(D.P, D.B);
+    for (size_t i = 0; i < gpp.size(); i++) c->enc_spec.A.a[i] = gpp[i] ? 1 : 0;
+  } else {
+    rc = build_code(kind, k, d, n, w, c->def, err);
+    if (rc) return fail(rc, err);
+    c->enc_spec.A = c->def.Gpp;
+  }
   // encode plan: inputs = data blocks (slot 0), outputs = parity rows (slot 1), A = G''
   const CodeDef &D = c->def;
   c->enc_spec.n_slots = 2;
   for (int i = 0; i < D.B; i++) c->enc_spec.inputs.push_back({{{0, i, 1}}});
   for (int r = 0; r < D.P; r++) c->enc_spec.outputs.push_back({1, r});
-  c->enc_spec.A = D.Gpp;
   (void)generate_source(c->enc_spec, c->gen, c->enc_stats);  // XOR-program statistics
   // compile now if a device is present (the paper's initialization); else on first use
   int ndev = 0;
@@ -292,10 +311,12 @@ int pmrc_info(const pmrc_code *c, pmrc_info_t *o) {
   memset(o, 0, sizeof(*o));
   o->kind = D.kind; o->n = D.n; o->k = D.k; o->d = D.d; o->w = 8;
   o->alpha = D.alpha; o->B = D.B; o->parity_rows = D.P;
+  o->w = c->w;
+  const Mat &Apat = c->enc_spec.A;  // G'' (w = 16: its nonzero pattern)
   long nnz = 0;
-  for (uint8_t v : D.Gpp.a) nnz += v != 0;
+  for (uint8_t v : Apat.a) nnz += v != 0;
   o->nnz = (int)nnz;
-  o->zero_pct = D.Gpp.a.empty() ? 0.0 : 100.0 * (double)(D.Gpp.a.size() - nnz) / (double)D.Gpp.a.size();
+  o->zero_pct = Apat.a.empty() ? 0.0 : 100.0 * (double)(Apat.a.size() - nnz) / (double)Apat.a.size();
   o->repair_complete = D.repair_complete ? 1 : 0;
   o->xor_ops = c->enc_stats.xor2;
   o->xor_ops_naive = c->enc_stats.naive_lop3;
@@ -410,6 +431,7 @@ int pmrc_encode_source(const pmrc_code *c, char *buf, size_t cap, size_t *len) {
 }
 
 int pmrc_matrix(const pmrc_code *c, int which, uint8_t *buf, int *rows, int *cols) {
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
   if (!c || !rows || !cols) return fail(PMRC_EINVAL, "NULL argument");
   const CodeDef &D = c->def;
   const Mat *M = nullptr;
@@ -437,6 +459,7 @@ int pmrc_matrix(const pmrc_code *c, int which, uint8_t *buf, int *rows, int *col
 }
 
 int pmrc_layout(const pmrc_code *c, int *buf, int *rows, int *cols) {
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
   if (!c || !rows || !cols) return fail(PMRC_EINVAL, "NULL argument");
   *rows = c->def.Lrows;
   *cols = c->def.Lcols;
@@ -519,6 +542,7 @@ int pmrc_encode_host(pmrc_code *c, const void *data_host, void *parity_host, siz
 
 int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregion *pieces, void *data_out, size_t S,
                 size_t stripes, int *n_written, void *stream) {
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
   if (n_written) *n_written = 0;
   if (!c || !surv_ids || !pieces || !data_out) return fail(PMRC_EINVAL, "NULL argument");
   const CodeDef &D = c->def;
@@ -631,6 +655,7 @@ int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregio
 
 int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *in, size_t in_stride, void *out,
                size_t out_stride, size_t S, size_t stripes, void *stream) {
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
   if (!c || !A || !in || !out) return fail(PMRC_EINVAL, "NULL argument");
   if (rows < 1 || cols < 1 || rows > 4096 || cols > 4096) return fail(PMRC_EINVAL, "bad matrix shape");
   if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
@@ -676,6 +701,7 @@ int pmrc_set_max_ctas(pmrc_code *c, int max_ctas) {
 }
 
 int pmrc_read_cost(const pmrc_code *c, int lost_id, int *blocks) {
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
   if (!c || !blocks) return fail(PMRC_EINVAL, "NULL argument");
   if (lost_id < 0 || lost_id >= c->def.n) return fail(PMRC_EINVAL, "bad lost id");
   int cnt = 0;
@@ -685,6 +711,7 @@ int pmrc_read_cost(const pmrc_code *c, int lost_id, int *blocks) {
 }
 
 static int repair_common(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers, int *need) {
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
   const CodeDef &D = c->def;
   *need = (D.kind == KIND_RS) ? D.k : D.d;
   if (lost_id < 0 || lost_id >= D.n) return fail(PMRC_EINVAL, "bad lost id");
@@ -750,6 +777,7 @@ int pmrc_repair(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers,
 
 int pmrc_repair_project(pmrc_code *c, int lost_id, pmrc_cregion piece, pmrc_region beta, size_t S, size_t stripes,
                         void *stream) {
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
   if (!c) return fail(PMRC_EINVAL, "NULL handle");
   const CodeDef &D = c->def;
   if (lost_id < 0 || lost_id >= D.n) return fail(PMRC_EINVAL, "bad lost id");

@@ -123,6 +123,16 @@ static __device__ __forceinline__ void pm_pace_post(u64 *p, u64 v) {
 )CUDA";
 
 void coef_rows(uint8_t c, uint8_t rows[8]) { gf().bitmatrix(c, rows); }
+// W x W GF(2) matrix of "multiply by c" in GF(2^W) (W = 8 or 16), rows as masks over input bits
+void coef_rows_w(int W, uint32_t c, uint32_t rows[16]) {
+  if (W == 8) {
+    uint8_t r8[8];
+    gf().bitmatrix((uint8_t)c, r8);
+    for (int b = 0; b < 8; b++) rows[b] = r8[b];
+    return;
+  }
+  gf16().bitmatrix((uint16_t)c, rows);
+}
 
 // Emit an XOR program: base signal i is named base[i]; outputs into outs (assign or accumulate).
 // Statements (temps and output rows) are emitted by a greedy register-pressure-aware list
@@ -432,6 +442,10 @@ bool is_plain(const InputDesc &in) { return in.terms.size() == 1 && in.terms[0].
 
 std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st) {
   st = GenStats();
+  // symbol width: W bit planes per symbol; a warp handles a chunk of CB = 128 W bytes of every
+  // block (32 lanes x 32 symbols), a lane's 32 symbols are NSEG 16-byte segments 512 B apart
+  const int W = p.w == 16 ? 16 : 8;
+  const int CB = 128 * W, NSEG = W / 4;
   const int R = (int)p.outputs.size();
   const int C = (int)p.inputs.size();
   // ---- groups: output rows with identical support, split into chunks of max_rows ----
@@ -585,6 +599,23 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   std::ostringstream s;
   s << "// generated by libpmrc (codegen.cpp) — bitsliced GF(2^8) region linear combination\n";
   s << kHeader;
+  if (W == 16)
+    s << R"CUDA(// 16 words (32 GF(2^16) symbols, little-endian) <-> 16 bit planes; an involution (4 delta-swap stages)
+static __device__ __forceinline__ void pm_tr16(u32 *w) {
+  #pragma unroll
+  for (int i = 0; i < 8; i++) pm_sw(w[i], w[i + 8], 8, 0x00FF00FFu);
+  #pragma unroll
+  for (int h = 0; h < 16; h += 8)
+    #pragma unroll
+    for (int i = 0; i < 4; i++) pm_sw(w[h + i], w[h + i + 4], 4, 0x0F0F0F0Fu);
+  #pragma unroll
+  for (int h = 0; h < 16; h += 4)
+    #pragma unroll
+    for (int i = 0; i < 2; i++) pm_sw(w[h + i], w[h + i + 2], 2, 0x33333333u);
+  #pragma unroll
+  for (int h = 0; h < 16; h += 2) pm_sw(w[h], w[h + 1], 1, 0x55555555u);
+}
+)CUDA";
   s << "struct Slots { u64 ptr[" << std::max(1, p.n_slots) << "]; u64 stride[" << std::max(1, p.n_slots) << "]; };\n";
   s << "#define PM_QMAX " << qmax << "u\n";
   s << "#define PM_T " << T << "u\n";
@@ -624,6 +655,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   s << "\n// in-place 8x8 bit transpose of this lane's 32 bytes of blocks [lo, hi) of a stage buffer\n"
        "static __device__ __forceinline__ void pm_transpose_in(const u32 buf, const u32 lo, const u32 hi) {\n"
        "  #pragma unroll " << std::max(1, o.tr_unroll) << "\n";
+  if (W == 8)
   s << R"CUDA(  for (u32 i = lo; i < hi; i++) {
     const u32 a0 = buf + i * 1024u, a1 = a0 + 512u;
     const uint4 a = pm_lds(a0), b = pm_lds(a1);
@@ -631,6 +663,21 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     pm_tr8(w0, w1, w2, w3, w4, w5, w6, w7);
     pm_sts(a0, w0, w1, w2, w3);
     pm_sts(a1, w4, w5, w6, w7);
+  }
+}
+)CUDA";
+  else
+  s << R"CUDA(  for (u32 i = lo; i < hi; i++) {
+    const u32 a0 = buf + i * 2048u;
+    u32 w[16];
+    #pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const uint4 v = pm_lds(a0 + 512u * q);
+      w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
+    pm_tr16(w);
+    #pragma unroll
+    for (int q = 0; q < 4; q++) pm_sts(a0 + 512u * q, w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
   }
 }
 )CUDA";
@@ -643,10 +690,14 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     const int n = (int)sg.blocks.size();
     o2 << ind << "{ const u32 gq = " << gi << ";\n";
     o2 << ind << "  const u64 tt = pm_udiv(gq, dv_m, dv_s1, dv_s2);\n";
-    o2 << ind << "  const u64 qo = (u64)(gq - (u32)tt * chunks) * 1024u + lane * 16u;\n";
+    o2 << ind << "  const u64 qo = (u64)(gq - (u32)tt * chunks) * " << CB << "u + lane * 16u;\n";
     o2 << ind << "  const bool okq = " << valid << ";\n";
-    o2 << ind << "  const u32 z0 = (okq && qo < S) ? 16u : 0u, z1 = (okq && qo + 512u < S) ? 16u : 0u;\n";
-    o2 << ind << "  const u32 dst = sbuf + (" << bb << ") * (PM_QMAX * 1024u) + lane * 16u;\n";
+    if (NSEG == 2)
+      o2 << ind << "  const u32 z0 = (okq && qo < S) ? 16u : 0u, z1 = (okq && qo + 512u < S) ? 16u : 0u;\n";
+    else
+      for (int g4 = 0; g4 < NSEG; g4++)
+        o2 << ind << "  const u32 z" << g4 << " = (okq && qo + " << 512 * g4 << "u < S) ? 16u : 0u;\n";
+    o2 << ind << "  const u32 dst = sbuf + (" << bb << ") * (PM_QMAX * " << CB << "u) + lane * 16u;\n";
     o2 << ind << "  switch (rank) {\n";
     for (int rk = 0; rk < (WS ? NP : T); rk++) {
       const int lo = WS ? n * rk / NP : n * rk / T, hi = WS ? n * (rk + 1) / NP : n * (rk + 1) / T;
@@ -661,10 +712,11 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         o2 << ind << "    { const u64 a = sb" << bk.first << " + (u64)" << bk.second << "u * S;\n";
         // src_size 0 (chunk beyond S) zero-fills without reading the source
         const char *pol = sg.ef[i] == 1 ? "pol_ef" : (sg.ef[i] == 2 ? "pol_el" : "pol_en");
-        o2 << ind << "      pm_cp16(dst + " << i * 1024 << "u, (const void *)a, z0, " << pol
+        o2 << ind << "      pm_cp16(dst + " << i * CB << "u, (const void *)a, z0, " << pol
            << ");\n";
-        o2 << ind << "      pm_cp16(dst + " << i * 1024 + 512 << "u, (const void *)(a + 512u), z1, "
-           << pol << "); }\n";
+        for (int g4 = 1; g4 < NSEG; g4++)
+          o2 << ind << "      pm_cp16(dst + " << i * CB + 512 * g4 << "u, (const void *)(a + " << 512 * g4 << "u), z" << g4
+             << ", " << pol << ")" << (g4 + 1 == NSEG ? "; }" : ";") << "\n";
       }
       o2 << ind << "  } break;\n";
     }
@@ -681,15 +733,15 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
       long ones = 0;
       for (int r : groups[g].rows)
         for (int c : groups[g].cols)
-          if (uint8_t cf = p.A.at(r, c)) {
-            uint8_t br[8];
-            coef_rows(cf, br);
-            for (int b = 0; b < 8; b++) ones += __builtin_popcount(br[b]);
+          if (const uint32_t cf = p.coef(r, c)) {
+            uint32_t br[16];
+            coef_rows_w(W, cf, br);
+            for (int b = 0; b < W; b++) ones += __builtin_popcount(br[b]);
           }
       long nblk = 0;
       for (int c : groups[g].cols) nblk += (long)p.inputs[c].terms.size();
       // per-chunk cost: transposes (48 instructions per block), XOR work, fixed per-item overhead
-      const long w = 48 * (nblk + (long)groups[g].rows.size()) + (3 * ones) / 10 + 300;
+      const long w = 6L * W * (nblk + (long)groups[g].rows.size()) + (3 * ones) / 10 + 300;
       cw[g + 1] = cw[g] + w;
     }
     s << "__constant__ unsigned int pm_cw[" << cw.size() << "] = {";
@@ -719,7 +771,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
       s << "      case " << rk << ": {\n";
       std::vector<std::string> outs;
       for (int r = 0; r < m; r++)
-        for (int b = 0; b < 8; b++) outs.push_back("o" + std::to_string(r) + "_" + std::to_string(b));
+        for (int b = 0; b < W; b++) outs.push_back("o" + std::to_string(r) + "_" + std::to_string(b));
       if (!outs.empty()) {
         s << "        u32 ";
         for (size_t i = 0; i < outs.size(); i++) s << (i ? ", " : "") << outs[i];
@@ -734,7 +786,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         const int nblk = (int)sg.blocks.size();
         s << "        {\n";
         if (WS) {
-          s << "          const u32 buf = sbuf + pb * (PM_QMAX * 1024u);\n";
+          s << "          const u32 buf = sbuf + pb * (PM_QMAX * " << CB << "u);\n";
           if (rk < NP) {
             // producer: data landed -> transpose its share of the blocks -> FULL; wait until the
             // consumers released the other buffer (EMPTY) before loading the successor stage
@@ -752,7 +804,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         } else {
         // consume: own copies landed -> transpose own share -> team barrier
         s << "          pm_cp_wait<" << (D - 1) << ">();\n";
-        s << "          const u32 buf = sbuf + pb * (PM_QMAX * 1024u);\n";
+        s << "          const u32 buf = sbuf + pb * (PM_QMAX * " << CB << "u);\n";
         if (!(o.debug & 1))  // debug bit 0: skip the input transposes (timing experiments only: wrong results)
           s << "          pm_transpose_in(buf + lane * 16u, " << nblk * rk / T << "u, " << nblk * (rk + 1) / T << "u);\n";
         s << "          const u32 pl = buf + lane * 16u;\n";
@@ -768,13 +820,13 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         if (m == 0) emit_sync();
         if (m > 0) {
           std::vector<std::string> base;
-          std::vector<char> used_half(2 * nblk, 0);
+          std::vector<char> used_half(NSEG * nblk, 0);
           std::ostringstream body;
           for (size_t ci = 0; ci < sg.cols.size(); ci++) {
             const InputDesc &in = p.inputs[sg.cols[ci]];
             const int fb = sg.first_block[ci];
             if (is_plain(in)) {
-              for (int b = 0; b < 8; b++) base.push_back("P" + std::to_string(2 * fb + b / 4) + "." + comp[b % 4]);
+              for (int b = 0; b < W; b++) base.push_back("P" + std::to_string(NSEG * fb + b / 4) + "." + comp[b % 4]);
               continue;
             }
             std::string nm = "d" + std::to_string(ci);
@@ -804,23 +856,24 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
             for (size_t u = 0; u < in.terms.size(); u++) used_half[2 * (fb + u)] = used_half[2 * (fb + u) + 1] = 1;
             for (int b = 0; b < 8; b++) base.push_back(nm + "_" + std::to_string(b));
           }
-          std::vector<std::vector<int>> rows(8 * m);
+          std::vector<std::vector<int>> rows(W * m);
           for (int r = 0; r < m; r++)
             for (size_t ci = 0; ci < sg.cols.size(); ci++) {
-              uint8_t cf = p.A.at(G.rows[r0 + r], sg.cols[ci]);
+              const uint32_t cf = p.coef(G.rows[r0 + r], sg.cols[ci]);
               if (!cf) continue;
-              uint8_t br[8];
-              coef_rows(cf, br);
-              for (int b = 0; b < 8; b++)
-                for (int bp = 0; bp < 8; bp++)
-                  if ((br[b] >> bp) & 1) rows[r * 8 + b].push_back((int)ci * 8 + bp);
+              uint32_t br[16];
+              coef_rows_w(W, cf, br);
+              for (int b = 0; b < W; b++)
+                for (int bp = 0; bp < W; bp++)
+                  if ((br[b] >> bp) & 1) rows[r * W + b].push_back((int)ci * W + bp);
             }
           // the stage's network, optionally cut into sub-networks over net_in inputs each (CSE
           // within a sub-network only): temps and plane quads then die at sub-network boundaries,
           // which bounds register pressure for wide plans (decode) at the price of some sharing
           const int ncols = (int)sg.cols.size();
           // equal-sized sub-networks of at most net_in inputs (14 -> 7 + 7, 8 -> 4 + 4, not 7 + 1)
-          int sub = o.net_in > 0 ? o.net_in : ncols;
+          // (net_in counts GF(2^8) inputs: a GF(2^16) input has twice the planes)
+          int sub = o.net_in > 0 ? (W == 16 ? (o.net_in + 1) / 2 : o.net_in) : ncols;
           if (o.net_even && sub < ncols) {
             const int nsub = (ncols + sub - 1) / sub;
             sub = (ncols + nsub - 1) / nsub;
@@ -832,12 +885,12 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
             std::vector<std::vector<int>> sr(rows.size());
             for (size_t r = 0; r < rows.size(); r++)
               for (int x : rows[r])
-                if (x >= 8 * c0 && x < 8 * c1) sr[r].push_back(x - 8 * c0);
-            subs.push_back(make_slp(8 * (c1 - c0), sr, o.cse, o.cse_restarts));
-            sub_base.emplace_back(base.begin() + 8 * c0, base.begin() + 8 * c1);
+                if (x >= W * c0 && x < W * c1) sr[r].push_back(x - W * c0);
+            subs.push_back(make_slp(W * (c1 - c0), sr, o.cse, o.cse_restarts));
+            sub_base.emplace_back(base.begin() + W * c0, base.begin() + W * c1);
             const bool acc = !(first && c0 == 0);
-            st.xor2 += subs.back().xor2() + (acc ? 8 * m : 0);
-            st.xor2_naive += make_slp(8 * (c1 - c0), sr, false).xor2() + (acc ? 8 * m : 0);
+            st.xor2 += subs.back().xor2() + (acc ? W * m : 0);
+            st.xor2_naive += make_slp(W * (c1 - c0), sr, false).xor2() + (acc ? W * m : 0);
           }
           st.naive_lop3 += naive_lop3(rows);
           // sub-networks whose inputs are all plain blocks this warp transposed itself run before
@@ -854,7 +907,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
             }
             (own ? order_pre : order_post).push_back((int)si2);
           }
-          std::vector<char> loaded(2 * nblk, 0);
+          std::vector<char> loaded(NSEG * nblk, 0);
           int emitted = 0;
           auto emit_sub = [&](int si2) {
             std::ostringstream net;
@@ -863,7 +916,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
               int h = std::stoi(nmb.substr(1, nmb.find('.') - 1));
               if (loaded[h]) return;
               loaded[h] = 1;
-              net << "          const uint4 P" << h << " = pm_lds(pl + " << (h / 2) * 1024 + (h % 2) * 512 << "u);\n";
+              net << "          const uint4 P" << h << " = pm_lds(pl + " << (h / NSEG) * CB + (h % NSEG) * 512 << "u);\n";
             };
             const bool acc = !(first && emitted == 0);
             emitted++;
@@ -893,10 +946,10 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
           {
             // planes of derived inputs (fused repair projections) after the barrier
             std::ostringstream pre;
-            for (int h = 0; h < 2 * nblk; h++)
+            for (int h = 0; h < NSEG * nblk; h++)
               if (used_half[h] && !loaded[h]) {
                 loaded[h] = 1;
-                pre << "          const uint4 P" << h << " = pm_lds(pl + " << (h / 2) * 1024 + (h % 2) * 512 << "u);\n";
+                pre << "          const uint4 P" << h << " = pm_lds(pl + " << (h / NSEG) * CB + (h % NSEG) * 512 << "u);\n";
               }
             s << pre.str() << body.str();
           }
@@ -919,12 +972,24 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
       for (int r = 0; r < m; r++) {
         const OutputDesc &od = p.outputs[G.rows[r0 + r]];
         std::string n = "o" + std::to_string(r);
+        if (W == 8) {
         if (!(o.debug & 2))  // debug bit 1: skip the output transposes (timing experiments only)
         s << "        pm_tr8(" << n << "_0, " << n << "_1, " << n << "_2, " << n << "_3, " << n << "_4, " << n << "_5, "
           << n << "_6, " << n << "_7);\n";
         s << "        { unsigned char *pp = (unsigned char *)(ob" << od.slot << " + (u64)" << od.blk << "u * S);\n";
         s << "          pm_st(pp + o0, v0, " << n << "_0, " << n << "_1, " << n << "_2, " << n << "_3, pol_ef);\n";
         s << "          pm_st(pp + o1, v1, " << n << "_4, " << n << "_5, " << n << "_6, " << n << "_7, pol_ef); }\n";
+        } else {
+          s << "        { u32 wv[16] = {";
+          for (int b = 0; b < 16; b++) s << (b ? ", " : "") << n << "_" << b;
+          s << "};\n";
+          if (!(o.debug & 2)) s << "          pm_tr16(wv);\n";
+          s << "          unsigned char *pp = (unsigned char *)(ob" << od.slot << " + (u64)" << od.blk << "u * S);\n";
+          for (int q4 = 0; q4 < 4; q4++)
+            s << "          pm_st(pp + o" << q4 << ", v" << q4 << ", wv[" << 4 * q4 << "], wv[" << 4 * q4 + 1 << "], wv["
+              << 4 * q4 + 2 << "], wv[" << 4 * q4 + 3 << "], pol_ef);\n";
+          s << "        }\n";
+        }
         st.transposes++;
       }
       s << "      } break;\n";
@@ -939,7 +1004,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   s << "  const u32 total = stripes * chunks;\n";
   s << "  const u32 per_cta = (total + gridDim.x - 1u) / gridDim.x;\n";
   s << "  const u32 c0 = blockIdx.x * per_cta, c1 = min(total, c0 + per_cta);\n";
-  s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (" << NB << "u * PM_QMAX * 1024u);\n";
+  s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (" << NB << "u * PM_QMAX * " << CB << "u);\n";
   s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en(), pol_el = pm_policy_el();\n";
   s << "  u32 pb = 0u;\n";
   if (first_sid >= 0) {
@@ -966,8 +1031,13 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     s << "      const u32 gi = tb + m;\n";
     s << "      const u64 t = pm_udiv(gi, dv_m, dv_s1, dv_s2);\n";
     s << "      const u32 q = gi - (u32)t * chunks;\n";
-    s << "      const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
-    s << "      const bool v0 = o0 < S, v1 = o1 < S;\n";
+    if (W == 8) {
+      s << "      const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
+      s << "      const bool v0 = o0 < S, v1 = o1 < S;\n";
+    } else {
+      s << "      const u64 o0 = (u64)q * " << CB << "u + lane * 16u, o1 = o0 + 512u, o2 = o0 + 1024u, o3 = o0 + 1536u;\n";
+      s << "      const bool v0 = o0 < S, v1 = o1 < S, v2 = o2 < S, v3 = o3 < S;\n";
+    }
     emit_body(g, [&](size_t gg, size_t sj) {
       if (sj + 1 < gstages[gg].size()) {
         emit_issue(s, gstages[gg][sj + 1], "gi", "true", "pb ^ 1u", "          ");
@@ -995,7 +1065,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   // second read hits L2) and each SM only ever executes one group's code (instruction cache).
   // Teams interleave over the range (team, team + teams, ...) so all groups advance in step.
   s << "  const u32 teams = " << teams << "u;\n";
-  s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (" << NB << "u * PM_QMAX * 1024u);\n";
+  s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (" << NB << "u * PM_QMAX * " << CB << "u);\n";
   s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en(), pol_el = pm_policy_el();\n";
   s << "  u32 pb = 0u;\n";
   s << "  bool pacing = pace != 0;\n";
@@ -1060,8 +1130,13 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     }
     s << "      const u64 t = pm_udiv(gi, dv_m, dv_s1, dv_s2);\n";
     s << "      const u32 q = gi - (u32)t * chunks;\n";
-    s << "      const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
-    s << "      const bool v0 = o0 < S, v1 = o1 < S;\n";
+    if (W == 8) {
+      s << "      const u64 o0 = (u64)q * 1024u + lane * 16u, o1 = o0 + 512u;\n";
+      s << "      const bool v0 = o0 < S, v1 = o1 < S;\n";
+    } else {
+      s << "      const u64 o0 = (u64)q * " << CB << "u + lane * 16u, o1 = o0 + 512u, o2 = o0 + 1024u, o3 = o0 + 1536u;\n";
+      s << "      const bool v0 = o0 < S, v1 = o1 < S, v2 = o2 < S, v3 = o3 < S;\n";
+    }
     emit_body(g, [&](size_t gg, size_t sj) {
       const int ns = (int)gstages[gg].size();
       const int di = ((int)sj + D) / ns, sid = gstages[gg][((int)sj + D) % ns];
@@ -1104,7 +1179,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   }
   s << "}\n";
   }
-  st.smem_per_warp = (NB * qmax * 1024 + T - 1) / T;
+  st.smem_per_warp = (NB * qmax * CB + T - 1) / T;
   for (auto &gs : gstages) st.max_stages = std::max(st.max_stages, (int)gs.size());
   return s.str();
 }

@@ -248,3 +248,83 @@ int build_code(int kind, int k, int d, int n, int w, CodeDef &o, std::string &er
 }
 
 }  // namespace pmrc
+
+namespace pmrc {
+
+// GF(2^16) sparse PM-MSR, systematic parity part only (P:163-187 with the field of
+// reading R1b): the same Psi / L / G / G' = G Gtilde^{-1} pipeline as build_code, on 16-bit symbols.
+int build_gpp16(int k, int d, int n, int &alpha, int &B, std::vector<uint16_t> &gpp, std::string &err) {
+  const GF65536 &F = gf16();
+  if (k < 2 || d != 2 * k - 2) { err = "MSR requires k >= 2 and d = 2k-2"; return PMRC_EUNSUPPORTED; }
+  if (n <= d || n > 4096) { err = "MSR requires d < n <= 4096"; return PMRC_EINVAL; }
+  const int a = k - 1;
+  alpha = a;
+  B = k * a;
+  // Psi: x_i = g^{i+alpha} (1-based i), Phi = [I_alpha; 1/(x_i - y_j)], y_j = g^{j-1};
+  // Lambda_ii = (x_i - 1)/(x_i - g^alpha)
+  std::vector<uint16_t> psi((size_t)n * d), lam(n);
+  for (int i = 0; i < n; i++) {
+    const uint16_t x = F.gexp(i + 1 + a);
+    lam[i] = F.div(x ^ 1, x ^ F.gexp(a));
+    for (int j = 0; j < a; j++) {
+      const uint16_t phi = (i < a) ? (uint16_t)(i == j) : F.inv(x ^ F.gexp(j));
+      psi[(size_t)i * d + j] = phi;
+      psi[(size_t)i * d + a + j] = F.mul(lam[i], phi);
+    }
+  }
+  for (int i = 0; i < n; i++)
+    for (int i2 = 0; i2 < i; i2++)
+      if (lam[i] == lam[i2]) { err = "sparse MSR (GF(2^16)): Lambda values collide"; return PMRC_EUNSUPPORTED; }
+  // L: S1 then S2, row-major over each upper triangle (R4)
+  std::vector<int> L((size_t)d * a, 0);
+  int next = 1;
+  number_symmetric(L, a, 0, 0, a, next);
+  number_symmetric(L, a, a, 0, a, next);
+  // G (n alpha x B): G_{alpha i + j, L_{l,j}} = Psi_{i,l}
+  std::vector<uint16_t> G((size_t)n * a * B, 0);
+  for (int i = 0; i < n; i++)
+    for (int j = 0; j < a; j++)
+      for (int l = 0; l < d; l++) {
+        const int idx = L[(size_t)l * a + j];
+        if (idx) G[((size_t)i * a + j) * B + idx - 1] = psi[(size_t)i * d + l];
+      }
+  // Gtilde^{-1} by Gauss-Jordan
+  std::vector<uint16_t> Wm(G.begin(), G.begin() + (size_t)B * B), Inv((size_t)B * B, 0);
+  for (int i = 0; i < B; i++) Inv[(size_t)i * B + i] = 1;
+  for (int col = 0; col < B; col++) {
+    int piv = -1;
+    for (int r = col; r < B; r++)
+      if (Wm[(size_t)r * B + col]) { piv = r; break; }
+    if (piv < 0) { err = "Gtilde singular (GF(2^16))"; return PMRC_EUNSUPPORTED; }
+    if (piv != col)
+      for (int c = 0; c < B; c++) {
+        std::swap(Wm[(size_t)piv * B + c], Wm[(size_t)col * B + c]);
+        std::swap(Inv[(size_t)piv * B + c], Inv[(size_t)col * B + c]);
+      }
+    const uint16_t s = F.inv(Wm[(size_t)col * B + col]);
+    for (int c = 0; c < B; c++) {
+      Wm[(size_t)col * B + c] = F.mul(Wm[(size_t)col * B + c], s);
+      Inv[(size_t)col * B + c] = F.mul(Inv[(size_t)col * B + c], s);
+    }
+    for (int r = 0; r < B; r++) {
+      const uint16_t f = r == col ? 0 : Wm[(size_t)r * B + col];
+      if (!f) continue;
+      for (int c = 0; c < B; c++) {
+        Wm[(size_t)r * B + c] ^= F.mul(f, Wm[(size_t)col * B + c]);
+        Inv[(size_t)r * B + c] ^= F.mul(f, Inv[(size_t)col * B + c]);
+      }
+    }
+  }
+  // G'' = (parity rows of G) Gtilde^{-1}
+  const int P = (n - k) * a;
+  gpp.assign((size_t)P * B, 0);
+  for (int r = 0; r < P; r++)
+    for (int t = 0; t < B; t++) {
+      const uint16_t g = G[((size_t)k * a + r) * B + t];
+      if (!g) continue;
+      for (int c = 0; c < B; c++) gpp[(size_t)r * B + c] ^= F.mul(g, Inv[(size_t)t * B + c]);
+    }
+  return PMRC_OK;
+}
+
+}  // namespace pmrc

@@ -7,6 +7,11 @@ const GF256 &gf() {
   return g;
 }
 
+const GF65536 &gf16() {
+  static const GF65536 g;
+  return g;
+}
+
 Mat matmul(const Mat &A, const Mat &B) {
   const GF256 &F = gf();
   Mat C(A.r, B.c);

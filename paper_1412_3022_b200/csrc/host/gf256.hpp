@@ -48,6 +48,37 @@ struct GF256 {
 
 const GF256 &gf();
 
+// GF(2^16) for the w = 16 codes: x^16+x^12+x^3+x+1 (0x1100B), g = 2 (reading
+// R1b).  Log/antilog tables built by shift-and-reduce (x * 2 each step).
+struct GF65536 {
+  std::vector<uint16_t> exp_t;  // 2 * 65535 entries
+  std::vector<int> log_t;       // 65536 entries, log_t[0] = -1
+  GF65536() : exp_t(2 * 65535), log_t(65536, -1) {
+    uint32_t x = 1;
+    for (int e = 0; e < 65535; e++) {
+      exp_t[e] = (uint16_t)x;
+      log_t[x] = e;
+      x <<= 1;
+      if (x & 0x10000u) x ^= 0x1100Bu;
+    }
+    for (int e = 65535; e < 2 * 65535; e++) exp_t[e] = exp_t[e - 65535];
+  }
+  uint16_t mul(uint16_t a, uint16_t b) const { return (a && b) ? exp_t[log_t[a] + log_t[b]] : 0; }
+  uint16_t inv(uint16_t a) const { return exp_t[(65535 - log_t[a]) % 65535]; }
+  uint16_t div(uint16_t a, uint16_t b) const { return mul(a, inv(b)); }
+  uint16_t gexp(long e) const { return exp_t[((e % 65535) + 65535) % 65535]; }
+  // 16x16 GF(2) matrix of "multiply by c": row b is a 16-bit mask over input bits b'
+  void bitmatrix(uint16_t c, uint32_t rows[16]) const {
+    for (int b = 0; b < 16; b++) rows[b] = 0;
+    for (int bp = 0; bp < 16; bp++) {
+      const uint16_t col = mul(c, (uint16_t)(1u << bp));
+      for (int b = 0; b < 16; b++)
+        if ((col >> b) & 1) rows[b] |= 1u << bp;
+    }
+  }
+};
+const GF65536 &gf16();
+
 // dense byte matrix, row-major
 struct Mat {
   int r = 0, c = 0;

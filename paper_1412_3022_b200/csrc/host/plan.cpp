@@ -84,6 +84,7 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     oo.layout = (G <= sms && (sms % G) * 10 <= sms) ? 1 : 0;
     if (oo.layout == 1 && g0.group_cost_ratio > 1.2) oo.layout = 2;  // unequal groups: apportion CTAs
   }
+  if (p.w == 16 && oo.team == 2 && oo.max_rows == 8) oo.team = 4;  // 16 planes per row: 2 rows per warp
   if (oo.ws) {  // ws_prod producers + 2 consumers per team, <= 4 teams (4 named barriers each), 2 buffers
     oo.team = std::max(1, oo.ws_prod) + 2;
     oo.warps = oo.team * std::min(4, 12 / oo.team);
@@ -181,6 +182,7 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
   k.tpb = oo.tpb;
   k.chunk_loop = oo.chunk_loop;
   k.layout = oo.layout;
+  k.w = p.w == 16 ? 16 : 8;
   k.grid_ctas = oo.grid_ctas;
   k.teams = std::max(1, oo.warps / std::max(1, oo.team));
   k.smem = (size_t)k.stats.smem_per_warp * oo.warps;
@@ -249,7 +251,8 @@ static int oo_grid(const Kernel &k) { return k.grid_ctas; }
 int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides, size_t S, size_t stripes,
                   void *stream, std::string &err, int max_ctas) {
   if (S == 0 || stripes == 0) return PMRC_OK;
-  const uint64_t chunks64 = (S + 1023) / 1024;
+  const uint64_t cb = 128ull * (uint64_t)k.w;  // chunk bytes per block
+  const uint64_t chunks64 = (S + cb - 1) / cb;
   if (chunks64 > 0xFFFFFFFFull) { err = "S too large"; return PMRC_EINVAL; }
   const uint32_t chunks = (uint32_t)chunks64;
   // items = stripes * chunks * groups must fit in 32 bits: split launches over stripe ranges

@@ -33,7 +33,10 @@ struct PlanSpec {
   int n_slots = 0;
   std::vector<InputDesc> inputs;
   std::vector<OutputDesc> outputs;
-  Mat A;  // outputs x inputs
+  Mat A;  // outputs x inputs (w = 16: nonzero pattern only, coefficients in A16)
+  int w = 8;                   // symbol width: GF(2^8) bytes or GF(2^16) little-endian byte pairs
+  std::vector<uint16_t> A16;   // w = 16: outputs x inputs coefficients, row-major
+  uint32_t coef(int r, int c) const { return w == 16 ? A16[(size_t)r * A.c + c] : A.at(r, c); }
 };
 
 struct GenOptions {
@@ -94,6 +97,7 @@ struct Kernel {
   int tpb = 256;
   int chunk_loop = 1;
   int layout = 0;
+  int w = 8;                 // symbol width: chunk = 128 w bytes of every block per warp
   int grid_ctas = 148;
   int teams = 1;
   void *pace = nullptr;             // layout 1: per-(CTA, team) progress counters (device)

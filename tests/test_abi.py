@@ -61,7 +61,7 @@ def test_create_errors():
         pm.pmrc_create(pm.PMRC_MSR_SPARSE, 3, 3, 6)   # MSR needs d = 2k-2
     assert e.value.rc == pm.PMRC_EUNSUPPORTED
     with pytest.raises(pm.PmrcError) as e:
-        pm.pmrc_create(pm.PMRC_MSR_SPARSE, 8, 14, 16, w=16)
+        pm.pmrc_create(pm.PMRC_MSR_SPARSE, 8, 14, 16, w=12)        # only w = 8 and (encode) w = 16
     assert e.value.rc == pm.PMRC_EUNSUPPORTED
     with pytest.raises(pm.PmrcError) as e:
         pm.pmrc_create(pm.PMRC_MSR_VANILLA, 16, 30, 32)  # R8 lambda collision
@@ -147,3 +147,25 @@ def test_prepare_plans_parallel_without_gpu():
     assert rcs[str(pats[0])] == pm.PMRC_OK and rcs[str(pats[2])] == pm.PMRC_OK
     assert rcs[str(pats[1])] == pm.PMRC_ESINGULAR
     assert rcs[str(pats[3])] == pm.PMRC_EINVAL
+
+
+def test_gf16_code_host_side():
+    # w = 16: the sparse MSR code builds, keeps Table 1's sparsity, and every
+    # operation but encode is refused loudly
+    c = pm.pmrc_create(pm.PMRC_MSR_SPARSE, 8, 14, 16, w=16)
+    try:
+        info = pm.pmrc_info(c)
+        assert (info["w"], info["B"], info["parity_rows"], info["nnz"], info["zero_pct"]) == (16, 56, 56, 784, 75.0)
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_decode(c, list(range(8, 16)), [(16, 0)] * 8, 16, 32, 1)
+        assert e.value.rc == pm.PMRC_EUNSUPPORTED
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_matrix(c, pm.MATRIX_GPP)
+        assert e.value.rc == pm.PMRC_EUNSUPPORTED
+        assert "pm_tr16" in pm.pmrc_encode_source(c)
+    finally:
+        pm.pmrc_destroy(c)
+    for kind in (pm.PMRC_MSR_VANILLA, pm.PMRC_MBR, pm.PMRC_RS_VANDERMONDE):
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_create(kind, 8, 8 if kind == pm.PMRC_RS_VANDERMONDE else 14, 16, w=16)
+        assert e.value.rc == pm.PMRC_EUNSUPPORTED

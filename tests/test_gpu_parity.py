@@ -488,3 +488,22 @@ def test_distributed_repair_single_rank_with_product_kernels():
         assert torch.equal(out, st.piece_tensor(f))
     finally:
         st.close()
+
+
+@pytest.mark.parametrize("k,n,S,stripes", [(8, 16, 2048 + 48, 2), (4, 8, 4096, 3), (8, 15, 64, 5)])
+def test_encode_gf16_bit_exact(k, n, S, stripes):
+    # w = 16 extension: the GPU encode of the sparse MSR code over GF(2^16)
+    # (little-endian byte pairs) equals the GF(2^16) oracle (oracle/gf16.py); ragged chunk tails
+    import oracle.gf16 as G16
+    code = pm.pmrc_create(pm.PMRC_MSR_SPARSE, k, 2 * k - 2, n, w=16)
+    try:
+        info = pm.pmrc_info(code)
+        B, P = info["B"], info["parity_rows"]
+        x = inputs.stripe_data(stripes, B, S, seed=40 + k)
+        data = torch.from_numpy(x).to(DEV)
+        par = torch.full((stripes, P, S), 0xEE, dtype=torch.uint8, device=DEV)
+        pm.pmrc_encode(code, data.data_ptr(), par.data_ptr(), S, stripes, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(par.cpu().numpy(), G16.encode(n, k, x))
+    finally:
+        pm.pmrc_destroy(code)

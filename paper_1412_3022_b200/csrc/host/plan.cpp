@@ -75,6 +75,10 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
       if (oo.warps <= 0) oo.warps = 16;
     }
   }
+  if (p.w == 16) {  // 16 planes per row: groups of 4 rows (2 per warp), stages of <= 8 blocks of 2 KiB
+    if (oo.team == 2 && oo.max_rows == 8) oo.max_rows = 4;      // measured: k=8 0.54 -> 0.74 TB/s
+    if (oo.in_block == 16) oo.in_block = 8;
+  }
   if (oo.layout < 0) {
     // group-specialised CTAs when the groups tile the 148 SMs with <= 10% left idle
     GenStats g0;
@@ -84,7 +88,6 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     oo.layout = (G <= sms && (sms % G) * 10 <= sms) ? 1 : 0;
     if (oo.layout == 1 && g0.group_cost_ratio > 1.2) oo.layout = 2;  // unequal groups: apportion CTAs
   }
-  if (p.w == 16 && oo.team == 2 && oo.max_rows == 8) oo.team = 4;  // 16 planes per row: 2 rows per warp
   if (oo.ws) {  // ws_prod producers + 2 consumers per team, <= 4 teams (4 named barriers each), 2 buffers
     oo.team = std::max(1, oo.ws_prod) + 2;
     oo.warps = oo.team * std::min(4, 12 / oo.team);

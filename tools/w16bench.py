@@ -13,5 +13,5 @@ for k, n in ((8, 16), (4, 8)):
     ms = timed(lambda: pm.pmrc_encode(c, data.data_ptr(), par.data_ptr(), S, stripes, st), 10)
     ps = pm.pmrc_plan_stats(c, 2)
     alu = ps['naive_lop3'] * (S // 64) * stripes / (148 * 64 * 1.965e9)
-    print(json.dumps({'w': 16, 'k': k, 'n': n, 'ms': round(ms, 4), 'GBps': round(stripes * B * S / ms / 1e6, 1), 'alu_roof_frac': round(alu / (ms * 1e-3), 3)}))
+    print(json.dumps({'gen': os.environ.get('PMRC_GEN', ''), 'w': 16, 'k': k, 'n': n, 'ms': round(ms, 4), 'GBps': round(stripes * B * S / ms / 1e6, 1), 'alu_roof_frac': round(alu / (ms * 1e-3), 3)}))
     pm.pmrc_destroy(c)

@@ -73,6 +73,25 @@ def _precompile_one(args):
     return args, rc
 
 
+# decode plans of fixed failure patterns the GPU tests use (GF(2^16): NVRTC takes 30-80 s each)
+# (kind, k, d, n, w, survivor ids)
+PRECOMPILE_DECODE = [(0, 8, 14, 16, 16, (0, 1, 4, 5, 9, 12, 14, 15)), (0, 8, 14, 16, 16, tuple(range(8, 16)))]
+
+
+def _precompile_decode(args):
+    import ctypes
+    L = ctypes.CDLL(LIB)
+    h = ctypes.c_void_p()
+    kind, k, d, n, w, ids = args
+    rc = L.pmrc_create(ctypes.byref(h), kind, k, d, n, w)
+    if rc == 0:
+        arr = (ctypes.c_int * len(ids))(*ids)
+        n_ = ctypes.c_size_t(0)
+        rc = L.pmrc_plan_source(h, 0, 0, arr, len(ids), 1, None, ctypes.c_size_t(0), ctypes.byref(n_))
+        L.pmrc_destroy(h)
+    return args, rc
+
+
 def precompile(configs=PRECOMPILE, clean=True):
     """NVRTC-compile the encode kernels of `configs` into paper_1412_3022_b200/kcache (no GPU).
     clean=True first drops cubins of earlier generator versions (the cache is keyed by source)."""
@@ -84,6 +103,7 @@ def precompile(configs=PRECOMPILE, clean=True):
                 os.remove(os.path.join(kdir, f))
     with get_context("spawn").Pool(min(len(configs), os.cpu_count() or 4)) as pool:
         res = pool.map(_precompile_one, configs)
+        res += pool.map(_precompile_decode, PRECOMPILE_DECODE)
     bad = [r for r in res if r[1] != 0]
     if bad:
         raise RuntimeError("precompile failed: %s" % bad)

@@ -431,7 +431,7 @@ int pmrc_encode_source(const pmrc_code *c, char *buf, size_t cap, size_t *len) {
 }
 
 int pmrc_matrix(const pmrc_code *c, int which, uint8_t *buf, int *rows, int *cols) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode and decode only (SURVEY NEXT-4)");
   if (!c || !rows || !cols) return fail(PMRC_EINVAL, "NULL argument");
   const CodeDef &D = c->def;
   const Mat *M = nullptr;
@@ -459,7 +459,7 @@ int pmrc_matrix(const pmrc_code *c, int which, uint8_t *buf, int *rows, int *col
 }
 
 int pmrc_layout(const pmrc_code *c, int *buf, int *rows, int *cols) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode and decode only (SURVEY NEXT-4)");
   if (!c || !rows || !cols) return fail(PMRC_EINVAL, "NULL argument");
   *rows = c->def.Lrows;
   *cols = c->def.Lcols;
@@ -540,9 +540,118 @@ int pmrc_encode_host(pmrc_code *c, const void *data_host, void *parity_host, siz
   return PMRC_OK;
 }
 
+// GF(2^16) decode plan (w = 16): the same rule as the GF(2^8) plan in pmrc_decode (R13):
+// greedy B independent rows of G' = [I_B; G''], systematic survivors first, then the inverse's
+// rows of the data blocks no surviving systematic node holds.  Returns 0, PMRC_ESINGULAR, or 1 if
+// nothing is missing.
+static int decode_spec16(const pmrc_code *c, const int *surv_ids, int n_surv, PlanSpec &spec) {
+  const CodeDef &D = c->def;
+  const GF65536 &F = gf16();
+  const int B = D.B, a = D.alpha;
+  const std::vector<uint16_t> &Gpp = c->enc_spec.A16;
+  auto row_of = [&](int node, int j, std::vector<uint16_t> &row) {
+    row.assign(B, 0);
+    if (node < D.k) row[node * a + j] = 1;
+    else for (int x = 0; x < B; x++) row[x] = Gpp[(size_t)((node - D.k) * a + j) * B + x];
+  };
+  std::vector<int> order;
+  for (int pass = 0; pass < 2; pass++)
+    for (int id = 0; id < D.n; id++) {
+      if ((pass == 0) != (id < D.k)) continue;
+      for (int q = 0; q < n_surv; q++)
+        if (surv_ids[q] == id) order.push_back(q);
+    }
+  std::vector<std::vector<uint16_t>> basis, selrows;
+  std::vector<int> pivcol;
+  std::vector<std::pair<int, int>> sel;
+  std::vector<uint16_t> row;
+  for (int q : order)
+    for (int j = 0; j < a && (int)sel.size() < B; j++) {
+      row_of(surv_ids[q], j, row);
+      std::vector<uint16_t> red = row;
+      for (size_t bi = 0; bi < basis.size(); bi++) {
+        const uint16_t f = red[pivcol[bi]];
+        if (!f) continue;
+        for (int x = 0; x < B; x++) red[x] ^= F.mul(f, basis[bi][x]);
+      }
+      int pc = -1;
+      for (int x = 0; x < B; x++)
+        if (red[x]) { pc = x; break; }
+      if (pc < 0) continue;
+      const uint16_t sc = F.inv(red[pc]);
+      for (int x = 0; x < B; x++) red[x] = F.mul(red[x], sc);
+      for (size_t bi = 0; bi < basis.size(); bi++) {
+        const uint16_t f = basis[bi][pc];
+        if (!f) continue;
+        for (int x = 0; x < B; x++) basis[bi][x] ^= F.mul(f, red[x]);
+      }
+      basis.push_back(red);
+      pivcol.push_back(pc);
+      selrows.push_back(row);
+      sel.push_back({q, j});
+    }
+  if ((int)sel.size() < B) return PMRC_ESINGULAR;
+  // invert the selected rows (Gauss-Jordan)
+  std::vector<uint16_t> Wm((size_t)B * B), Inv((size_t)B * B, 0);
+  for (int r = 0; r < B; r++) {
+    for (int x = 0; x < B; x++) Wm[(size_t)r * B + x] = selrows[r][x];
+    Inv[(size_t)r * B + r] = 1;
+  }
+  for (int col = 0; col < B; col++) {
+    int piv = -1;
+    for (int r = col; r < B; r++)
+      if (Wm[(size_t)r * B + col]) { piv = r; break; }
+    if (piv < 0) return PMRC_ESINGULAR;
+    if (piv != col)
+      for (int x = 0; x < B; x++) {
+        std::swap(Wm[(size_t)piv * B + x], Wm[(size_t)col * B + x]);
+        std::swap(Inv[(size_t)piv * B + x], Inv[(size_t)col * B + x]);
+      }
+    const uint16_t sc = F.inv(Wm[(size_t)col * B + col]);
+    for (int x = 0; x < B; x++) {
+      Wm[(size_t)col * B + x] = F.mul(Wm[(size_t)col * B + x], sc);
+      Inv[(size_t)col * B + x] = F.mul(Inv[(size_t)col * B + x], sc);
+    }
+    for (int r = 0; r < B; r++) {
+      const uint16_t f = r == col ? 0 : Wm[(size_t)r * B + col];
+      if (!f) continue;
+      for (int x = 0; x < B; x++) {
+        Wm[(size_t)r * B + x] ^= F.mul(f, Wm[(size_t)col * B + x]);
+        Inv[(size_t)r * B + x] ^= F.mul(f, Inv[(size_t)col * B + x]);
+      }
+    }
+  }
+  std::vector<char> held(B, 0);
+  for (int q = 0; q < n_surv; q++)
+    if (surv_ids[q] < D.k)
+      for (int j = 0; j < a; j++) held[surv_ids[q] * a + j] = 1;
+  std::vector<int> missing, used;
+  for (int x = 0; x < B; x++)
+    if (!held[x]) missing.push_back(x);
+  if (missing.empty()) return 1;
+  for (int x = 0; x < B; x++) {
+    bool nz = false;
+    for (int m : missing) nz |= Inv[(size_t)m * B + x] != 0;
+    if (nz) used.push_back(x);
+  }
+  spec = PlanSpec();
+  spec.n_slots = n_surv + 1;
+  spec.w = 16;
+  for (int x : used) spec.inputs.push_back({{{sel[x].first, sel[x].second, 1}}});
+  for (int m : missing) spec.outputs.push_back({n_surv, m});
+  spec.A = Mat((int)missing.size(), (int)used.size());
+  spec.A16.assign(missing.size() * used.size(), 0);
+  for (size_t r = 0; r < missing.size(); r++)
+    for (size_t x = 0; x < used.size(); x++) {
+      const uint16_t v = Inv[(size_t)missing[r] * B + used[x]];
+      spec.A16[r * used.size() + x] = v;
+      spec.A.at((int)r, (int)x) = v ? 1 : 0;
+    }
+  return PMRC_OK;
+}
+
 int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregion *pieces, void *data_out, size_t S,
                 size_t stripes, int *n_written, void *stream) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
   if (n_written) *n_written = 0;
   if (!c || !surv_ids || !pieces || !data_out) return fail(PMRC_EINVAL, "NULL argument");
   const CodeDef &D = c->def;
@@ -551,7 +660,22 @@ int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregio
   const std::string key = ids_key("dec", surv_ids, n_surv, 0);
   auto fe = c->plan_err.find(key);
   if (fe != c->plan_err.end()) return fail(fe->second, "survivors do not span the data (cached)");
-  if (c->dry || !c->plan_meta.count(key)) {
+  if (c->w == 16 && (c->dry || !c->plan_meta.count(key))) {
+    PlanSpec spec;
+    const int r16 = decode_spec16(c, surv_ids, n_surv, spec);
+    if (r16 == PMRC_ESINGULAR) {
+      c->plan_err[key] = PMRC_ESINGULAR;
+      return fail(PMRC_ESINGULAR, "survivors do not span the data");
+    }
+    if (r16 == 1) {
+      c->plan_meta[key] = 0;
+      return PMRC_OK;
+    }
+    Kernel *Kb = nullptr;
+    int rc = get_kernel(c, key, spec, &Kb);
+    if (rc) return rc;
+    c->plan_meta[key] = (int)spec.outputs.size();
+  } else if (c->dry || !c->plan_meta.count(key)) {
     PlanSpec spec;
     {
       // ---- plan (R13): greedy B independent rows of G', systematic survivors first ----
@@ -655,7 +779,7 @@ int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregio
 
 int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *in, size_t in_stride, void *out,
                size_t out_stride, size_t S, size_t stripes, void *stream) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode and decode only (SURVEY NEXT-4)");
   if (!c || !A || !in || !out) return fail(PMRC_EINVAL, "NULL argument");
   if (rows < 1 || cols < 1 || rows > 4096 || cols > 4096) return fail(PMRC_EINVAL, "bad matrix shape");
   if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
@@ -701,7 +825,7 @@ int pmrc_set_max_ctas(pmrc_code *c, int max_ctas) {
 }
 
 int pmrc_read_cost(const pmrc_code *c, int lost_id, int *blocks) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode and decode only (SURVEY NEXT-4)");
   if (!c || !blocks) return fail(PMRC_EINVAL, "NULL argument");
   if (lost_id < 0 || lost_id >= c->def.n) return fail(PMRC_EINVAL, "bad lost id");
   int cnt = 0;
@@ -711,7 +835,7 @@ int pmrc_read_cost(const pmrc_code *c, int lost_id, int *blocks) {
 }
 
 static int repair_common(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers, int *need) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode and decode only (SURVEY NEXT-4)");
   const CodeDef &D = c->def;
   *need = (D.kind == KIND_RS) ? D.k : D.d;
   if (lost_id < 0 || lost_id >= D.n) return fail(PMRC_EINVAL, "bad lost id");
@@ -777,7 +901,7 @@ int pmrc_repair(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers,
 
 int pmrc_repair_project(pmrc_code *c, int lost_id, pmrc_cregion piece, pmrc_region beta, size_t S, size_t stripes,
                         void *stream) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode only (SURVEY NEXT-4)");
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode and decode only (SURVEY NEXT-4)");
   if (!c) return fail(PMRC_EINVAL, "NULL handle");
   const CodeDef &D = c->def;
   if (lost_id < 0 || lost_id >= D.n) return fail(PMRC_EINVAL, "bad lost id");

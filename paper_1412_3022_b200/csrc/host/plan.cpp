@@ -68,7 +68,7 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     if (p0.layout < 0) p0.layout = 0;
     GenStats w0;
     (void)generate_source(p, p0, w0);
-    if (o.auto_wide && w0.clustered && w0.max_stages >= 3 && p.outputs.size() > 8 && oo.team == 2 &&
+    if (o.auto_wide && p.w != 16 && w0.clustered && w0.max_stages >= 3 && p.outputs.size() > 8 && oo.team == 2 &&
         oo.max_rows == 8) {
       oo.max_rows = 16;
       oo.team = 4;

@@ -507,3 +507,28 @@ def test_encode_gf16_bit_exact(k, n, S, stripes):
         assert np.array_equal(par.cpu().numpy(), G16.encode(n, k, x))
     finally:
         pm.pmrc_destroy(code)
+
+
+@pytest.mark.parametrize("ids", [[0, 1, 4, 5, 9, 12, 14, 15], list(range(8, 16))])
+def test_decode_gf16(ids):
+    # w = 16: decode from a survivor set returns the data (unique result) -- the GF(2^16)
+    # oracle's decode round trip pins the same algebra on the CPU (tests/test_oracle_gf16.py)
+    k, n, S, stripes = 8, 16, 2048 + 48, 2
+    code = pm.pmrc_create(pm.PMRC_MSR_SPARSE, k, 14, n, w=16)
+    try:
+        info = pm.pmrc_info(code)
+        B, P, a = info["B"], info["parity_rows"], info["alpha"]
+        data = torch.from_numpy(inputs.stripe_data(stripes, B, S, seed=71)).to(DEV)
+        par = torch.empty((stripes, P, S), dtype=torch.uint8, device=DEV)
+        st = torch.cuda.current_stream().cuda_stream
+        pm.pmrc_encode(code, data.data_ptr(), par.data_ptr(), S, stripes, st)
+        pieces = [(par.data_ptr() + (i - k) * a * S, P * S) if i >= k else (data.data_ptr() + i * a * S, B * S)
+                  for i in ids]
+        out = torch.zeros_like(data)
+        nw = pm.pmrc_decode(code, ids, pieces, out.data_ptr(), S, stripes, st)
+        torch.cuda.synchronize()
+        miss = [i * a + x for i in range(k) if i not in ids for x in range(a)]
+        assert nw == len(miss)
+        assert torch.equal(out[:, miss], data[:, miss])
+    finally:
+        pm.pmrc_destroy(code)

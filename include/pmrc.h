@@ -91,7 +91,7 @@ typedef struct {
 /* Build the code: Psi, L, G, G' = G Gtilde^{-1}, G''; generate and compile the encode
  * kernel for the CUDA device current at the call (the paper's "initialization").
  * w = 8 (GF(2^8), every operation), or w = 16 for the sparse MSR code (GF(2^16), polynomial 0x1100B,
- * little-endian byte-pair symbols; encode and decode).  For RS d is ignored (taken = k).  *out receives a handle to free with
+ * little-endian byte-pair symbols; encode, decode and fused repair).  For RS d is ignored (taken = k).  *out receives a handle to free with
  * pmrc_destroy. */
 int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w);
 void pmrc_destroy(pmrc_code *c);

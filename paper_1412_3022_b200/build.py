@@ -73,21 +73,24 @@ def _precompile_one(args):
     return args, rc
 
 
-# decode plans of fixed failure patterns the GPU tests use (GF(2^16): NVRTC takes 30-80 s each)
-# (kind, k, d, n, w, survivor ids)
-PRECOMPILE_DECODE = [(0, 8, 14, 16, 16, (0, 1, 4, 5, 9, 12, 14, 15)), (0, 8, 14, 16, 16, tuple(range(8, 16)))]
+# decode (op 0) / repair (op 1) plans of fixed failure patterns the GPU tests use (GF(2^16): NVRTC
+# takes 20-80 s each).  (kind, k, d, n, w, op, lost id, node ids)
+PRECOMPILE_DECODE = [(0, 8, 14, 16, 16, 0, 0, (0, 1, 4, 5, 9, 12, 14, 15)),
+                     (0, 8, 14, 16, 16, 0, 0, tuple(range(8, 16))),
+                     (0, 8, 14, 16, 16, 1, 15, (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 11, 12, 13, 14)),
+                     (0, 8, 14, 16, 16, 1, 3, (0, 1, 2, 4, 5, 6, 7, 8, 9, 10, 12, 13, 14, 15))]
 
 
 def _precompile_decode(args):
     import ctypes
     L = ctypes.CDLL(LIB)
     h = ctypes.c_void_p()
-    kind, k, d, n, w, ids = args
+    kind, k, d, n, w, op, lost, ids = args
     rc = L.pmrc_create(ctypes.byref(h), kind, k, d, n, w)
     if rc == 0:
         arr = (ctypes.c_int * len(ids))(*ids)
         n_ = ctypes.c_size_t(0)
-        rc = L.pmrc_plan_source(h, 0, 0, arr, len(ids), 1, None, ctypes.c_size_t(0), ctypes.byref(n_))
+        rc = L.pmrc_plan_source(h, op, lost, arr, len(ids), 1, None, ctypes.c_size_t(0), ctypes.byref(n_))
         L.pmrc_destroy(h)
     return args, rc
 

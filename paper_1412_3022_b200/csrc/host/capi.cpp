@@ -48,7 +48,8 @@ struct pmrc_code {
   std::map<std::string, int> plan_err;                   // cached failures (ESINGULAR)
   std::map<std::string, int> plan_meta;                  // e.g. blocks written by a decode plan
   HostStage hs;
-  int w = 8;                   // symbol width (16: GF(2^16) encode only)
+  int w = 8;                   // symbol width (16: GF(2^16) encode, decode, repair)
+  std::vector<uint16_t> psi16, lam16;  // w = 16: Psi (n x d) and Lambda (n)
   int max_ctas = 0;            // pmrc_set_max_ctas: grid cap for every launch (0 = one full wave)
   std::string *dry = nullptr;  // pmrc_plan_source: get_kernel stores the generated source here instead
   PlanSpec dry_spec;           //   and the plan
@@ -254,7 +255,7 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
     if (kind != KIND_MSR_SPARSE) return fail(PMRC_EUNSUPPORTED, "w = 16: only the sparse MSR code (kind 0)");
     int alpha = 0, B = 0;
     std::vector<uint16_t> gpp;
-    rc = build_gpp16(k, d, n, alpha, B, gpp, err);
+    rc = build_gpp16(k, d, n, alpha, B, gpp, err, &c->psi16, &c->lam16);
     if (rc) return fail(rc, err);
     CodeDef &D = c->def;
     D.kind = kind; D.n = n; D.k = k; D.d = d; D.alpha = alpha; D.B = B; D.P = (n - k) * alpha;
@@ -431,7 +432,7 @@ int pmrc_encode_source(const pmrc_code *c, char *buf, size_t cap, size_t *len) {
 }
 
 int pmrc_matrix(const pmrc_code *c, int which, uint8_t *buf, int *rows, int *cols) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode and decode only (SURVEY NEXT-4)");
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode, decode and repair (SURVEY NEXT-4)");
   if (!c || !rows || !cols) return fail(PMRC_EINVAL, "NULL argument");
   const CodeDef &D = c->def;
   const Mat *M = nullptr;
@@ -459,7 +460,7 @@ int pmrc_matrix(const pmrc_code *c, int which, uint8_t *buf, int *rows, int *col
 }
 
 int pmrc_layout(const pmrc_code *c, int *buf, int *rows, int *cols) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode and decode only (SURVEY NEXT-4)");
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode, decode and repair (SURVEY NEXT-4)");
   if (!c || !rows || !cols) return fail(PMRC_EINVAL, "NULL argument");
   *rows = c->def.Lrows;
   *cols = c->def.Lcols;
@@ -779,7 +780,7 @@ int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregio
 
 int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *in, size_t in_stride, void *out,
                size_t out_stride, size_t S, size_t stripes, void *stream) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode and decode only (SURVEY NEXT-4)");
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode, decode and repair (SURVEY NEXT-4)");
   if (!c || !A || !in || !out) return fail(PMRC_EINVAL, "NULL argument");
   if (rows < 1 || cols < 1 || rows > 4096 || cols > 4096) return fail(PMRC_EINVAL, "bad matrix shape");
   if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
@@ -825,7 +826,7 @@ int pmrc_set_max_ctas(pmrc_code *c, int max_ctas) {
 }
 
 int pmrc_read_cost(const pmrc_code *c, int lost_id, int *blocks) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode and decode only (SURVEY NEXT-4)");
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode, decode and repair (SURVEY NEXT-4)");
   if (!c || !blocks) return fail(PMRC_EINVAL, "NULL argument");
   if (lost_id < 0 || lost_id >= c->def.n) return fail(PMRC_EINVAL, "bad lost id");
   int cnt = 0;
@@ -835,7 +836,6 @@ int pmrc_read_cost(const pmrc_code *c, int lost_id, int *blocks) {
 }
 
 static int repair_common(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers, int *need) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode and decode only (SURVEY NEXT-4)");
   const CodeDef &D = c->def;
   *need = (D.kind == KIND_RS) ? D.k : D.d;
   if (lost_id < 0 || lost_id >= D.n) return fail(PMRC_EINVAL, "bad lost id");
@@ -858,7 +858,66 @@ int pmrc_repair(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers,
   auto fe = c->plan_err.find(key);
   if (fe != c->plan_err.end()) return fail(fe->second, "helper matrix singular (cached)");
   Kernel *K = nullptr;
-  if (c->dry || !c->plans.count(key)) {
+  if (c->w == 16 && (c->dry || !c->plans.count(key))) {
+    // GF(2^16) (w = 16): mu = phi_f (P:53 footnote), R = [I_alpha | lambda_f I_alpha] Psi_H^{-1}
+    const GF65536 &F = gf16();
+    const int dd = D.d, a = D.alpha;
+    std::vector<uint16_t> Wm((size_t)dd * dd), Inv((size_t)dd * dd, 0);
+    for (int r = 0; r < dd; r++) {
+      for (int x = 0; x < dd; x++) Wm[(size_t)r * dd + x] = c->psi16[(size_t)helper_ids[r] * dd + x];
+      Inv[(size_t)r * dd + r] = 1;
+    }
+    for (int col = 0; col < dd; col++) {
+      int piv = -1;
+      for (int r = col; r < dd; r++)
+        if (Wm[(size_t)r * dd + col]) { piv = r; break; }
+      if (piv < 0) {
+        c->plan_err[key] = PMRC_ESINGULAR;
+        return fail(PMRC_ESINGULAR, "Psi_H singular for this (lost, helpers) pair (DESIGN.md R10)");
+      }
+      if (piv != col)
+        for (int x = 0; x < dd; x++) {
+          std::swap(Wm[(size_t)piv * dd + x], Wm[(size_t)col * dd + x]);
+          std::swap(Inv[(size_t)piv * dd + x], Inv[(size_t)col * dd + x]);
+        }
+      const uint16_t sc = F.inv(Wm[(size_t)col * dd + col]);
+      for (int x = 0; x < dd; x++) {
+        Wm[(size_t)col * dd + x] = F.mul(Wm[(size_t)col * dd + x], sc);
+        Inv[(size_t)col * dd + x] = F.mul(Inv[(size_t)col * dd + x], sc);
+      }
+      for (int r = 0; r < dd; r++) {
+        const uint16_t f = r == col ? 0 : Wm[(size_t)r * dd + col];
+        if (!f) continue;
+        for (int x = 0; x < dd; x++) {
+          Wm[(size_t)r * dd + x] ^= F.mul(f, Wm[(size_t)col * dd + x]);
+          Inv[(size_t)r * dd + x] ^= F.mul(f, Inv[(size_t)col * dd + x]);
+        }
+      }
+    }
+    const uint16_t lf = c->lam16[lost_id];
+    PlanSpec spec;
+    spec.w = 16;
+    spec.n_slots = n_helpers + 1;
+    for (int h = 0; h < n_helpers; h++) {
+      InputDesc in;
+      for (int b = 0; b < a; b++) {
+        const uint16_t mu = c->psi16[(size_t)lost_id * dd + b];
+        if (mu) in.terms.push_back({h, b, mu});
+      }
+      spec.inputs.push_back(in);
+    }
+    for (int q = 0; q < a; q++) spec.outputs.push_back({n_helpers, q});
+    spec.A = Mat(a, n_helpers);
+    spec.A16.assign((size_t)a * n_helpers, 0);
+    for (int q = 0; q < a; q++)
+      for (int h = 0; h < n_helpers; h++) {
+        const uint16_t v = Inv[(size_t)q * dd + h] ^ F.mul(lf, Inv[(size_t)(a + q) * dd + h]);
+        spec.A16[(size_t)q * n_helpers + h] = v;
+        spec.A.at(q, h) = v ? 1 : 0;
+      }
+    rc = get_kernel(c, key, spec, &K);
+    if (rc) return rc;
+  } else if (c->dry || !c->plans.count(key)) {
     Mat R;
     if (!repair_matrix(D, lost_id, helper_ids, R)) {
       c->plan_err[key] = PMRC_ESINGULAR;
@@ -901,7 +960,7 @@ int pmrc_repair(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers,
 
 int pmrc_repair_project(pmrc_code *c, int lost_id, pmrc_cregion piece, pmrc_region beta, size_t S, size_t stripes,
                         void *stream) {
-  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode and decode only (SURVEY NEXT-4)");
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode, decode and repair (SURVEY NEXT-4)");
   if (!c) return fail(PMRC_EINVAL, "NULL handle");
   const CodeDef &D = c->def;
   if (lost_id < 0 || lost_id >= D.n) return fail(PMRC_EINVAL, "bad lost id");
@@ -940,6 +999,7 @@ int pmrc_repair_project(pmrc_code *c, int lost_id, pmrc_cregion piece, pmrc_regi
 
 int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers, const pmrc_cregion *betas,
                         pmrc_region out_piece, size_t S, size_t stripes, void *stream) {
+  if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode, decode and repair (SURVEY NEXT-4)");
   if (!c || !helper_ids || !betas) return fail(PMRC_EINVAL, "NULL argument");
   int need = 0;
   int rc = repair_common(c, lost_id, helper_ids, n_helpers, &need);

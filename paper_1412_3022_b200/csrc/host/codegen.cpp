@@ -831,15 +831,15 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
             }
             std::string nm = "d" + std::to_string(ci);
             std::vector<std::string> dbase;
-            std::vector<std::vector<int>> drows(8);
+            std::vector<std::vector<int>> drows(W);
             for (size_t u = 0; u < in.terms.size(); u++) {
               const int bi = fb + (int)u;
-              uint8_t br[8];
-              coef_rows(in.terms[u].coef, br);
-              for (int bb = 0; bb < 8; bb++) {
-                dbase.push_back("P" + std::to_string(2 * bi + bb / 4) + "." + comp[bb % 4]);
-                for (int bp = 0; bp < 8; bp++)
-                  if ((br[bb] >> bp) & 1) drows[bb].push_back((int)u * 8 + bp);
+              uint32_t br[16];
+              coef_rows_w(W, in.terms[u].coef, br);
+              for (int bb = 0; bb < W; bb++) {
+                dbase.push_back("P" + std::to_string(NSEG * bi + bb / 4) + "." + comp[bb % 4]);
+                for (int bp = 0; bp < W; bp++)
+                  if ((br[bb] >> bp) & 1) drows[bb].push_back((int)u * W + bp);
               }
             }
             Slp ds = make_slp((int)dbase.size(), drows, o.cse, o.cse_restarts);
@@ -848,13 +848,15 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
               st.naive_lop3 += naive_lop3(drows);
               st.xor2_naive += make_slp((int)dbase.size(), drows, false).xor2();
             }
-            body << "          u32 " << nm << "_0, " << nm << "_1, " << nm << "_2, " << nm << "_3, " << nm << "_4, " << nm
-                 << "_5, " << nm << "_6, " << nm << "_7;\n";
+            body << "          u32 ";
+            for (int bb = 0; bb < W; bb++) body << (bb ? ", " : "") << nm << "_" << bb;
+            body << ";\n";
             std::vector<std::string> dout;
-            for (int bb = 0; bb < 8; bb++) dout.push_back(nm + "_" + std::to_string(bb));
+            for (int bb = 0; bb < W; bb++) dout.push_back(nm + "_" + std::to_string(bb));
             emit_slp(body, ds, dbase, dout, false, nm + "t");
-            for (size_t u = 0; u < in.terms.size(); u++) used_half[2 * (fb + u)] = used_half[2 * (fb + u) + 1] = 1;
-            for (int b = 0; b < 8; b++) base.push_back(nm + "_" + std::to_string(b));
+            for (size_t u = 0; u < in.terms.size(); u++)
+              for (int g4 = 0; g4 < NSEG; g4++) used_half[NSEG * (fb + u) + g4] = 1;
+            for (int b = 0; b < W; b++) base.push_back(nm + "_" + std::to_string(b));
           }
           std::vector<std::vector<int>> rows(W * m);
           for (int r = 0; r < m; r++)

@@ -253,7 +253,8 @@ namespace pmrc {
 
 // GF(2^16) sparse PM-MSR, systematic parity part only (P:163-187 with the field of
 // reading R1b): the same Psi / L / G / G' = G Gtilde^{-1} pipeline as build_code, on 16-bit symbols.
-int build_gpp16(int k, int d, int n, int &alpha, int &B, std::vector<uint16_t> &gpp, std::string &err) {
+int build_gpp16(int k, int d, int n, int &alpha, int &B, std::vector<uint16_t> &gpp, std::string &err,
+                std::vector<uint16_t> *psi_out, std::vector<uint16_t> *lam_out) {
   const GF65536 &F = gf16();
   if (k < 2 || d != 2 * k - 2) { err = "MSR requires k >= 2 and d = 2k-2"; return PMRC_EUNSUPPORTED; }
   if (n <= d || n > 4096) { err = "MSR requires d < n <= 4096"; return PMRC_EINVAL; }
@@ -275,6 +276,8 @@ int build_gpp16(int k, int d, int n, int &alpha, int &B, std::vector<uint16_t> &
   for (int i = 0; i < n; i++)
     for (int i2 = 0; i2 < i; i2++)
       if (lam[i] == lam[i2]) { err = "sparse MSR (GF(2^16)): Lambda values collide"; return PMRC_EUNSUPPORTED; }
+  if (psi_out) *psi_out = psi;
+  if (lam_out) *lam_out = lam;
   // L: S1 then S2, row-major over each upper triangle (R4)
   std::vector<int> L((size_t)d * a, 0);
   int next = 1;

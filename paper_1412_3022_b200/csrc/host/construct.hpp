@@ -31,6 +31,7 @@ struct CodeDef {
 // returns 0 or a PMRC_E* code; err receives a description
 int build_code(int kind, int k, int d, int n, int w, CodeDef &out, std::string &err);
 // GF(2^16) sparse MSR (w = 16): alpha, B and the systematic parity matrix G'' ((n-k) alpha x B)
-int build_gpp16(int k, int d, int n, int &alpha, int &B, std::vector<uint16_t> &gpp, std::string &err);
+int build_gpp16(int k, int d, int n, int &alpha, int &B, std::vector<uint16_t> &gpp, std::string &err,
+                std::vector<uint16_t> *psi_out = nullptr, std::vector<uint16_t> *lam_out = nullptr);
 
 }  // namespace pmrc

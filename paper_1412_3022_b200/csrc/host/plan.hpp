@@ -20,7 +20,7 @@ namespace pmrc {
 
 struct Term {
   int slot, blk;
-  uint8_t coef;
+  uint16_t coef;  // GF(2^8) or, for w = 16 plans, GF(2^16)
 };
 struct InputDesc {
   std::vector<Term> terms;  // one term with coef 1 = plain block

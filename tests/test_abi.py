@@ -150,14 +150,14 @@ def test_prepare_plans_parallel_without_gpu():
 
 
 def test_gf16_code_host_side():
-    # w = 16: the sparse MSR code builds, keeps Table 1's sparsity; encode and
-    # decode run, every other operation is refused loudly
+    # w = 16: the sparse MSR code builds, keeps Table 1's sparsity; encode, decode
+    # and fused repair run, the other operations are refused loudly
     c = pm.pmrc_create(pm.PMRC_MSR_SPARSE, 8, 14, 16, w=16)
     try:
         info = pm.pmrc_info(c)
         assert (info["w"], info["B"], info["parity_rows"], info["nnz"], info["zero_pct"]) == (16, 56, 56, 784, 75.0)
         with pytest.raises(pm.PmrcError) as e:
-            pm.pmrc_repair(c, 15, list(range(14)), [(16, 0)] * 14, (16, 0), 32, 1)
+            pm.pmrc_repair_project(c, 15, (16, 0), (16, 0), 32, 1)
         assert e.value.rc == pm.PMRC_EUNSUPPORTED
         with pytest.raises(pm.PmrcError) as e:
             pm.pmrc_matrix(c, pm.MATRIX_GPP)

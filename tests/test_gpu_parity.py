@@ -532,3 +532,35 @@ def test_decode_gf16(ids):
         assert torch.equal(out[:, miss], data[:, miss])
     finally:
         pm.pmrc_destroy(code)
+
+
+def test_repair_gf16():
+    # w = 16: exact repair (P:53 footnote) of a parity node (alpha blocks per helper) and a
+    # systematic node (1 block per helper); the R10 singular set is singular over GF(2^16) too
+    k, n, S, stripes = 8, 16, 2048 + 48, 2
+    code = pm.pmrc_create(pm.PMRC_MSR_SPARSE, k, 14, n, w=16)
+    try:
+        info = pm.pmrc_info(code)
+        B, P, a = info["B"], info["parity_rows"], info["alpha"]
+        data = torch.from_numpy(inputs.stripe_data(stripes, B, S, seed=72)).to(DEV)
+        par = torch.empty((stripes, P, S), dtype=torch.uint8, device=DEV)
+        st = torch.cuda.current_stream().cuda_stream
+        pm.pmrc_encode(code, data.data_ptr(), par.data_ptr(), S, stripes, st)
+
+        def piece(i):
+            return (par.data_ptr() + (i - k) * a * S, P * S) if i >= k else (data.data_ptr() + i * a * S, B * S)
+
+        def piece_t(i):
+            return par[:, (i - k) * a:(i - k + 1) * a] if i >= k else data[:, i * a:(i + 1) * a]
+        for f, omit in ((15, 10), (3, 11)):
+            H = [i for i in range(n) if i not in (f, omit)]
+            out = torch.zeros((stripes, a, S), dtype=torch.uint8, device=DEV)
+            pm.pmrc_repair(code, f, H, [piece(i) for i in H], (out.data_ptr(), a * S), S, stripes, st)
+            torch.cuda.synchronize()
+            assert torch.equal(out, piece_t(f)), f
+        H = [i for i in range(n) if i not in (0, 1)]
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_repair(code, 0, H, [piece(i) for i in H], (16 * 1024, a * S), S, stripes, st)
+        assert e.value.rc == pm.PMRC_ESINGULAR
+    finally:
+        pm.pmrc_destroy(code)

@@ -97,7 +97,7 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
   GenStats probe;
   (void)generate_source(p, oo, probe);
   int budget = 220 * 1024;
-  int w = std::max(1, std::min(16, budget / std::max(1, probe.smem_per_warp)));
+  int w = std::max(1, std::min(32, budget / std::max(1, probe.smem_per_warp)));
   // 12 warps (6 teams of 2): measured best for encode, and for the multi-stage repair plans
   // (config-4 repair 0.421 -> 0.404 ms vs 8 warps); wide decode plans set 16 above (auto_wide)
   int want = oo.warps;

@@ -193,11 +193,11 @@ int pmrc_plan_stats(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids
 /* The same for the plan pmrc_apply would run for matrix A (rows x cols). */
 int pmrc_apply_stats(pmrc_code *c, const uint8_t *A, int rows, int cols, pmrc_plan_stats_t *out);
 
-/* Diagnostics of the encode kernel's CTA pacing (group-specialised layout): copies the device
- * counter area (5 x E u64: progress counters, then per-(CTA, team) start / end globaltimer ns, ns
- * spent pacing and (group << 32 | pacing timeouts), the last four only with PMRC_GEN=trace=1) to host[0..cap) and
- * its length to *n (0 if the encode kernel has no counters).  Synchronous (cudaMemcpy); not part
- * of the data path. */
+/* Diagnostics of CTA pacing / timing (group-specialised layouts) of the last launched kernel that
+ * has counters (PMRC_GEN=trace=1 or pace_lag): copies the device counter area (5 x E u64: progress
+ * counters, then per-(CTA, team) start / end globaltimer ns, ns spent pacing and (group << 32 |
+ * pacing timeouts)) to host[0..cap) and its length to *n (0 if no launched kernel has counters).
+ * Synchronous (cudaMemcpy); not part of the data path. */
 int pmrc_debug_counters(const pmrc_code *c, unsigned long long *host, size_t cap, size_t *n);
 
 /* Number of kernels this library launched since load (for the bench's gpu_launches claim). */

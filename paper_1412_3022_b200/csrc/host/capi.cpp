@@ -50,6 +50,7 @@ struct pmrc_code {
   HostStage hs;
   int w = 8;                   // symbol width (16: GF(2^16) encode, decode, repair)
   std::vector<uint16_t> psi16, lam16;  // w = 16: Psi (n x d) and Lambda (n)
+  const Kernel *traced = nullptr;  // the last launched kernel with pacing / trace counters
   int max_ctas = 0;            // pmrc_set_max_ctas: grid cap for every launch (0 = one full wave)
   std::string *dry = nullptr;  // pmrc_plan_source: get_kernel stores the generated source here instead
   PlanSpec dry_spec;           //   and the plan
@@ -222,7 +223,8 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "warps" && v >= 1) c->gen.warps = v;
         if (key == "cse") c->gen.cse = v != 0;
         if (key == "sync_groups") c->gen.sync_groups = v != 0;
-        if (key == "sync_every") c->gen.sync_every = v;
+        if (key == "cta_sync") c->gen.cta_sync = v;
+        if (key == "dyn") c->gen.dyn = v;
         if (key == "ld_hint") c->gen.ld_hint = v;
         if (key == "chunk_loop" && v > 0) c->gen.chunk_loop = v;
         if (key == "team" && v > 0) c->gen.team = v;
@@ -335,11 +337,12 @@ int pmrc_precompile(const pmrc_code *c) {
 int pmrc_debug_counters(const pmrc_code *c, unsigned long long *host, size_t cap, size_t *n) {
   if (!c || !n) return fail(PMRC_EINVAL, "NULL argument");
   *n = 0;
-  if (!c->enc_built || !c->enc.pace) return PMRC_OK;
-  const size_t total = c->enc.pace_entries * 6;
+  const Kernel *K = c->traced;  // the last launched kernel that has counters
+  if (!K) return PMRC_OK;
+  const size_t total = K->pace_entries * 6;
   *n = total;
   if (!host || cap < total) return PMRC_OK;
-  if (cudaMemcpy(host, c->enc.pace, total * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+  if (cudaMemcpy(host, K->pace, total * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
     cudaGetLastError();
     return fail(PMRC_ECUDA, "cudaMemcpy(pace counters)");
   }
@@ -481,6 +484,7 @@ int pmrc_encode(pmrc_code *c, const void *data, void *parity, size_t S, size_t s
   uint64_t ptrs[2] = {(uint64_t)(uintptr_t)data, (uint64_t)(uintptr_t)parity};
   uint64_t strides[2] = {(uint64_t)D.B * S, (uint64_t)D.P * S};
   std::string err;
+  if (c->enc.pace) c->traced = &c->enc;
   rc = launch_kernel(c->enc, ptrs, strides, S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
   return PMRC_OK;
@@ -530,7 +534,8 @@ int pmrc_encode_host(pmrc_code *c, const void *data_host, void *parity_host, siz
     uint64_t ptrs[2] = {(uint64_t)(uintptr_t)h.d_data[b], (uint64_t)(uintptr_t)h.d_par[b]};
     uint64_t strides[2] = {in_b, out_b};
     std::string err;
-    rc = launch_kernel(c->enc, ptrs, strides, S, ns, st, err, c->max_ctas);
+    if (c->enc.pace) c->traced = &c->enc;
+  rc = launch_kernel(c->enc, ptrs, strides, S, ns, st, err, c->max_ctas);
     if (rc) return fail(rc, err);
     if (cudaMemcpyAsync((uint8_t *)parity_host + s0 * out_b, h.d_par[b], ns * out_b, cudaMemcpyDeviceToHost, st) !=
         cudaSuccess)
@@ -773,6 +778,7 @@ int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregio
   ptrs[n_surv] = (uint64_t)(uintptr_t)data_out;
   strides[n_surv] = (uint64_t)D.B * S;
   std::string err;
+  if (K->pace) c->traced = K;
   rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
   return PMRC_OK;
@@ -814,6 +820,7 @@ int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *i
   uint64_t ptrs[2] = {(uint64_t)(uintptr_t)in, (uint64_t)(uintptr_t)out};
   uint64_t strides[2] = {(uint64_t)in_stride, (uint64_t)out_stride};
   std::string err;
+  if (K->pace) c->traced = K;
   rc = launch_kernel(*K, ptrs, strides, S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
   return PMRC_OK;
@@ -953,6 +960,7 @@ int pmrc_repair(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers,
   ptrs[n_helpers] = (uint64_t)(uintptr_t)out_piece.ptr;
   strides[n_helpers] = out_piece.stripe_stride;
   std::string err;
+  if (K->pace) c->traced = K;
   rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
   return PMRC_OK;
@@ -992,6 +1000,7 @@ int pmrc_repair_project(pmrc_code *c, int lost_id, pmrc_cregion piece, pmrc_regi
   uint64_t ptrs[2] = {(uint64_t)(uintptr_t)piece.ptr, (uint64_t)(uintptr_t)beta.ptr};
   uint64_t strides[2] = {piece.stripe_stride, beta.stripe_stride};
   std::string err;
+  if (K->pace) c->traced = K;
   rc = launch_kernel(*K, ptrs, strides, S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
   return PMRC_OK;
@@ -1039,6 +1048,7 @@ int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids, int n_
   ptrs[n_helpers] = (uint64_t)(uintptr_t)out_piece.ptr;
   strides[n_helpers] = out_piece.stripe_stride;
   std::string err;
+  if (K->pace) c->traced = K;
   rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
   return PMRC_OK;

@@ -479,6 +479,9 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     int nleft = R;
     groups.clear();
     st.clustered = true;
+    // equal group sizes (28 rows, max 16 -> 14 + 14, not 16 + 12): group-specialised CTAs get equal
+    // chunk ranges, so unequal groups would leave the SMs of the small ones idle at the end
+    const int cap = (int)((R + min_groups - 1) / min_groups);
     while (nleft > 0) {
       int seed = -1;
       for (int r = 0; r < R; r++)
@@ -488,7 +491,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
       g.rows.push_back(seed);
       left[seed] = 0;
       nleft--;
-      while ((int)g.rows.size() < o.max_rows && nleft > 0) {
+      while ((int)g.rows.size() < cap && nleft > 0) {
         int best = -1, bgrow = 1 << 30;
         for (int r = 0; r < R; r++) {
           if (!left[r]) continue;
@@ -750,8 +753,11 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
   }
   const int TPB = 32 * std::max(T, o.warps);
   const int teams = TPB / 32 / T;
+  // dynamic chunk schedule (layout 1): teams take their next chunk from a per-group counter
+  const bool DYN = o.dyn > 0 && o.layout == 1 && !WS && NB == 2 && o.pace_lag == 0 && o.cta_sync == 0;
   s << "extern \"C\" __global__ void __launch_bounds__(" << TPB << ", 1) pmrc_kernel(const __grid_constant__ Slots R, "
-       "const u64 S, const u32 stripes, const u32 chunks, u64 *__restrict__ pace, const u32 epoch) {\n";
+       "const u64 S, const u32 stripes, const u32 chunks, u64 *__restrict__ pace, const u32 epoch"
+    << (DYN ? ", u32 *__restrict__ dyn" : "") << ") {\n";
   s << "  extern __shared__ __align__(1024) unsigned char pm_smem[];\n";
   s << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, team = warp / PM_T, rank = warp - team * PM_T;\n";
   s << "  u32 dv_m, dv_s1, dv_s2;\n  pm_udiv_setup(chunks, dv_m, dv_s1, dv_s2);\n";
@@ -1089,11 +1095,46 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
     s << "  const u32 spg = gridDim.x / " << groups.size() << "u, g = blockIdx.x / spg, r = blockIdx.x - g * spg;\n";
     s << "  const u32 total = stripes * chunks;\n";
     s << "  const u32 c0 = (u32)((u64)total * r / spg), c1 = (u32)((u64)total * (r + 1u) / spg);\n";
+    if (DYN) s << "  __shared__ u32 pm_nx[" << 4 * teams << "];\n";
   }
+  // dyn = 2 (steal): a team whose group has no chunks left goes on to the other groups' counters
+  const bool STEAL = DYN && o.dyn >= 2 && groups.size() > 1;
+  if (STEAL)
+    s << "  for (u32 hop = 0; hop < " << groups.size() << "u; hop++) {\n"
+      << "  const u32 gh = g + hop < " << groups.size() << "u ? g + hop : g + hop - " << groups.size() << "u;\n"
+      << "  switch (gh) {\n";
+  else
   s << "  switch (g) {\n";
   for (size_t g = 0; g < groups.size(); g++) {
     s << "  case " << g << ": {\n";
-    {
+    if (DYN) {
+      // team tau = r * teams + team of the group's NT teams starts at chunk tau; every further
+      // chunk comes from the group's counter (NT + atomicAdd), taken by rank 0 at the start of an
+      // item and passed to the team through shared memory (read after the item's first barrier)
+      s << "    const u32 NT = spg * teams;\n";
+      s << "    u32 *const dctr = dyn + 2u * " << g << "u;\n";
+      if (STEAL) {
+        // a visiting team starts from the counter too (broadcast through the team barrier, which
+        // also keeps the team's last buffer from being overwritten while a rank still reads it)
+        s << "    pb = 0u;\n";
+        s << "    u32 tau = r * teams + team;\n";
+        s << "    if (hop != 0u) {\n";
+        // (own slots, double-buffered by hop: a rank may still read the loop slots or the previous
+        // hop's slot when rank 0 gets here)
+        s << "      const u32 hs = 2u * teams + 2u * team + (hop & 1u);\n";
+        s << "      if (rank == 0u && lane == 0u) pm_nx[hs] = NT + atomicAdd(dctr, 1u);\n";
+        s << "      " << (T > 1 ? "pm_team_sync(1u + team, PM_T * 32u);" : "__syncwarp();") << "\n";
+        s << "      tau = pm_nx[hs];\n";
+        s << "    }\n";
+      } else
+        s << "    const u32 tau = r * teams + team;\n";
+      if (!gstages[g].empty()) {
+        s << "    if (tau < total) {\n";
+        emit_issue(s, gstages[g][0], "tau", "true", "0u", "      ");
+        s << "    }\n";
+      }
+      s << "    pm_cp_commit();\n";
+    } else {
       const int ns = (int)gstages[g].size();
       for (int pp = 0; pp < D; pp++) {
         if (ns) {
@@ -1107,6 +1148,21 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
       }
     }
     s << "    #pragma unroll 1\n";
+    const bool csync = o.cta_sync > 0 && o.layout == 1 && !WS;
+    if (csync) {
+      // every team runs the same number of iterations (the last one possibly idle) so that the
+      // CTA barrier at the top of each item is reached by all warps
+      s << "    for (u32 gb = c0, kk = 0; gb < c1; gb += teams, kk++) {\n";
+      s << "      const u32 gi = gb + team;\n";
+      s << "      __syncthreads();\n";
+      s << "      if (gi >= c1) continue;\n";
+    } else if (DYN) {
+      // rank 0 takes its counter value one item ahead (the atomic's L2 round trip overlaps a whole
+      // item): item kk publishes the value taken during item kk - 1
+      s << "    u32 nxt = (rank == 0u && lane == 0u) ? NT + atomicAdd(dctr, 1u) : 0u;\n";
+      s << "    for (u32 gi = tau, kk = 0; gi < total; kk++) {\n";
+      s << "      if (rank == 0u && lane == 0u) { pm_nx[2u * team + (kk & 1u)] = nxt; nxt = NT + atomicAdd(dctr, 1u); }\n";
+    } else
     s << "    for (u32 gi = c0 + team, kk = 0; gi < c1; gi += teams, kk++) {\n";
     const int pace_lag = o.layout == 1 ? o.pace_lag : 0;  // pacing assumes aligned (layout 1) ranges
     const bool pace_async = pace_lag > 0 && groups.size() <= 32;
@@ -1148,11 +1204,19 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
         emit_issue(s, sid, "gi", "true", bb, "          ");
         return;
       }
+      if (DYN) {
+        s << "          { const u32 nx = pm_nx[2u * team + (kk & 1u)];\n";
+        s << "          if (nx < total) {\n";
+        emit_issue(s, sid, "nx", "true", bb, "            ");
+        s << "          } }\n";
+        return;
+      }
       const std::string it = "gi + " + std::to_string(di) + "u * teams";
       s << "          if (" << it << " < c1) {\n";
       emit_issue(s, sid, it, "true", bb, "            ");
       s << "          }\n";
     });
+    if (DYN) s << "      gi = pm_nx[2u * team + (kk & 1u)];\n";
     if (pace_lag > 0)
       s << "      if (pace && rank == 0u && lane == 0u) pm_pace_post(pace + blockIdx.x * teams + team, ((u64)epoch << 32) | (kk + 1u));\n";
     if (pace_async) {
@@ -1165,18 +1229,22 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
       s << "        }\n      }\n";
     }
     s << "    }\n";
+    if (DYN)  // the group's last team to finish resets its counters for a later launch (slot ring)
+      s << "    if (rank == 0u && lane == 0u) { __threadfence(); if (atomicAdd(dctr + 1, 1u) == "
+        << (STEAL ? "gridDim.x * teams" : "NT") << " - 1u) { atomicExch(dctr, 0u); atomicExch(dctr + 1, 0u); } }\n";
     if (WS)  // balance the last EMPTY arrival of the consumers (the producer's final wait)
       s << "    if (rank < " << NP << "u && c0 + team < c1) pm_team_sync(4u * team + 2u + (pb ^ 1u), PM_T * 32u);\n";
     s << "  } break;\n";
   }
   s << "  default: break;\n  }\n";
+  if (STEAL) s << "  }\n";  // hop loop
   if (o.layout == 2) s << "  }\n";  // segment loop
   if (o.trace) {
     // diagnostics (E = 4096 entries per field, plan.cpp): [E + i] start, [2E + i] end (globaltimer ns),
-    // [3E + i] ns spent pacing, [4E + i] = group << 32 | pacing timeouts
+    // [3E + i] ns spent pacing, [4E + i] = smid << 48 | group << 32 | pacing timeouts
     s << "  if (pace && rank == 0u && lane == 0u) {\n";
     s << "    const u32 E = 4096u, i = blockIdx.x * teams + team;\n";
-    s << "    pace[E + i] = tr_t0; pace[2u * E + i] = pm_gtime(); pace[3u * E + i] = tr_wait; pace[4u * E + i] = ((u64)g << 32) | tr_fail;\n";
+    s << "    pace[E + i] = tr_t0; pace[2u * E + i] = pm_gtime(); pace[3u * E + i] = tr_wait; u32 smid; asm volatile(\"mov.u32 %0, %%smid;\" : \"=r\"(smid)); pace[4u * E + i] = ((u64)smid << 48) | ((u64)g << 32) | tr_fail;\n";
     s << "  }\n";
   }
   s << "}\n";

@@ -75,6 +75,17 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
       if (oo.warps <= 0) oo.warps = 16;
     }
   }
+  if (oo.dyn < 0) {
+    // dynamic chunk schedule, with teams moving on to other groups' chunks when theirs are done,
+    // for clustered plans (decode: rows of G~^-1): measured config-4 decode 0.873 -> 0.681 ms
+    // (static ranges left whole TPCs finishing 35% late); the encode keeps static ranges (0.528 vs
+    // 0.542 / 0.548 ms with dyn = 1 / 2)
+    GenOptions p1 = oo;
+    if (p1.layout < 0) p1.layout = 0;
+    GenStats w1;
+    (void)generate_source(p, p1, w1);
+    oo.dyn = w1.clustered ? 2 : 0;
+  }
   if (p.w == 16) {  // 16 planes per row: groups of 4 rows (2 per warp), stages of <= 8 blocks of 2 KiB
     if (oo.team == 2 && oo.max_rows == 8) oo.max_rows = 4;      // measured: k=8 0.54 -> 0.74 TB/s
     if (oo.in_block == 16) oo.in_block = 8;
@@ -216,7 +227,9 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
   int regs = 0;
   D.FuncGetAttribute(&regs, CU_FUNC_ATTRIBUTE_NUM_REGS, fn);
   k.regs = regs;
-  if (k.smem > 48 * 1024) {
+  int static_smem = 0;  // e.g. the dynamic schedule's per-team slots
+  D.FuncGetAttribute(&static_smem, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, fn);
+  if (k.smem + (size_t)static_smem > 48 * 1024) {
     cr = D.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)k.smem);
     if (cr != CUDA_SUCCESS) { D.ModuleUnload(mod); err = "cuFuncSetAttribute(smem): " + cu_err(cr); return PMRC_ECUDA; }
   }
@@ -238,12 +251,27 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
       return PMRC_ENOMEM;
     }
   }
+  if (k.source.find("u32 *__restrict__ dyn)") != std::string::npos) {
+    // dynamic schedule: a ring of counter slots, one per launch (the last team of a group resets
+    // its slot), so launches of this plan on different streams do not share counters
+    const size_t bytes = (size_t)kDynSlots * 2 * k.n_groups * sizeof(uint32_t);
+    if (cudaMalloc(&k.dyn, bytes) != cudaSuccess || cudaMemset(k.dyn, 0, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      free_kernel(k);
+      err = "cudaMalloc(schedule counters)";
+      return PMRC_ENOMEM;
+    }
+    k.dyn_on = true;
+  }
   return PMRC_OK;
 }
 
 void free_kernel(Kernel &k) {
   if (k.pace) cudaFree(k.pace);
   k.pace = nullptr;
+  if (k.dyn) cudaFree(k.dyn);
+  k.dyn = nullptr;
+  k.dyn_on = false;
   if (k.module && drv().ok) drv().ModuleUnload((CUmodule)k.module);
   k.module = nullptr;
   k.function = nullptr;
@@ -288,7 +316,8 @@ int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides
     // pacing only when every CTA has its counters and can be co-resident
     void *pace = (k.pace && grid * k.teams <= k.pace_entries) ? k.pace : nullptr;
     const uint32_t epoch = ++k.epoch;
-    void *args[] = {buf.data(), &S64, (void *)&ns, (void *)&chunks, &pace, (void *)&epoch};
+    void *dyn = k.dyn_on ? (void *)((uint32_t *)k.dyn + (size_t)(epoch % kDynSlots) * 2 * k.n_groups) : nullptr;
+    void *args[] = {buf.data(), &S64, (void *)&ns, (void *)&chunks, &pace, (void *)&epoch, &dyn};
     CUresult cr = drv().LaunchKernel((CUfunction)k.function, (unsigned)grid, 1, 1, k.tpb, 1, 1, (unsigned)k.smem, (CUstream)stream, args,
                                  nullptr);
     if (cr != CUDA_SUCCESS) { err = "cuLaunchKernel: " + cu_err(cr); return PMRC_ECUDA; }

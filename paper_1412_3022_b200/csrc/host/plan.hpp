@@ -47,7 +47,11 @@ struct GenOptions {
   int tpb = 256;         // (derived) threads per CTA
   bool cse = true;       // Paar CSE (false: naive per-row XOR chains)
   bool sync_groups = true;  // __syncthreads() before each group: warps of a CTA execute the same code
-  int sync_every = 0;       // also sync every N emitted XOR statements (0 = off)
+  int dyn = -1;             // layout 1: dynamic chunk schedule (per-group counters) instead of static
+                            // ranges; 2: teams then help the other groups (-1 auto: 2 for clustered
+                            // plans, i.e. decode, else 0)
+  int cta_sync = 0;         // layout 1: all teams of a CTA start every item together (CTA barrier):
+                            // the teams then fetch the same instructions at about the same time
   int chunk_loop = 24;      // chunks per team per group (loop: instruction reuse)
   int team = 2;             // warps sharing one chunk's stage buffer (each computes 1/team of the rows)
   int ld_hint = 1;
@@ -71,6 +75,8 @@ struct GenOptions {
   bool trace = false;       // layout 1 diagnostics: per-team start/end/wait times (pmrc_debug_counters)
   int pace_lag = 0;         // layout 1: max chunks a team runs ahead of its peers (0 = no pacing)
 };
+
+constexpr int kDynSlots = 64;  // counter slots of the dynamic schedule (launches in flight per plan)
 
 struct GenStats {
   int groups = 0;
@@ -102,6 +108,8 @@ struct Kernel {
   int teams = 1;
   void *pace = nullptr;             // layout 1: per-(CTA, team) progress counters (device)
   size_t pace_entries = 0;
+  void *dyn = nullptr;              // layout 1 dynamic schedule: kDynSlots x n_groups x 2 u32 counters
+  bool dyn_on = false;
   mutable uint32_t epoch = 0;       // launch epoch (counters carry it, so they never need a reset)
   size_t smem = 0;
   int blocks_per_sm = 1;

@@ -129,6 +129,12 @@ def test_plan_stats_and_source_without_gpu():
         assert e.value.rc == pm.PMRC_EINVAL
         src = pm.pmrc_plan_source(c, 1, 15, [i for i in range(16) if i not in (15, 10)])
         assert "pmrc_kernel" in src and "lop3" in src
+        # schedules: the config-4 decode takes chunks from per-group counters (and helps the other
+        # group when its own run out); the encode keeps static, aligned chunk ranges
+        dsrc = pm.pmrc_plan_source(c, 0, 0, [0, 1, 4, 5, 9, 12, 14, 15])
+        assert "atomicAdd(dctr, 1u)" in dsrc and "for (u32 hop = 0; hop < 2u; hop++)" in dsrc
+        esrc = pm.pmrc_encode_source(c)
+        assert "atomicAdd" not in esrc and "c1 = (u32)((u64)total * (r + 1u) / spg)" in esrc
     finally:
         pm.pmrc_destroy(c)
 

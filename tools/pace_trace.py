@@ -33,7 +33,7 @@ per = collections.defaultdict(list)
 for i in range(E):
     if not c[E + i]:
         continue
-    g = c[4 * E + i] >> 32
+    g = (c[4 * E + i] >> 32) & 0xFFFF
     per[g].append(((c[E + i] - base) / 1e3, (c[2 * E + i] - base) / 1e3, c[3 * E + i] / 1e3, c[4 * E + i] & 0xFFFFFFFF))
 print(json.dumps({"kind": kind, "k": k, "S": S, "groups": len(per)}))
 for g in sorted(per):

@@ -225,6 +225,9 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "sync_groups") c->gen.sync_groups = v != 0;
         if (key == "cta_sync") c->gen.cta_sync = v;
         if (key == "dyn") c->gen.dyn = v;
+        if (key == "even_groups") c->gen.even_groups = v != 0;
+        if (key == "cluster_wide") c->gen.cluster_wide = v != 0;
+        if (key == "balance_ranks") c->gen.balance_ranks = v != 0;
         if (key == "ld_hint") c->gen.ld_hint = v;
         if (key == "chunk_loop" && v > 0) c->gen.chunk_loop = v;
         if (key == "team" && v > 0) c->gen.team = v;

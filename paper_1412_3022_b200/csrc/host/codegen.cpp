@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // Generator of the bitsliced sm_100a region-linear-combination kernels.
 //
 // Kernel design, driven by what the B200 measurements showed:
@@ -479,9 +481,10 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     int nleft = R;
     groups.clear();
     st.clustered = true;
-    // equal group sizes (28 rows, max 16 -> 14 + 14, not 16 + 12): group-specialised CTAs get equal
-    // chunk ranges, so unequal groups would leave the SMs of the small ones idle at the end
-    const int cap = (int)((R + min_groups - 1) / min_groups);
+    // even_groups: equal group sizes (28 rows, max 16 -> 14 + 14, not 16 + 12), for static equal
+    // chunk ranges; with the dynamic schedule 16 + 12 is better: 4 + 4 + 4 + 4 and 3 + 3 + 3 + 3 rows
+    // per team rank keep the team barriers balanced (14 rows: 3 + 4 + 3 + 4)
+    const int cap = o.even_groups ? (int)((R + min_groups - 1) / min_groups) : o.max_rows;
     while (nleft > 0) {
       int seed = -1;
       for (int r = 0; r < R; r++)
@@ -497,7 +500,9 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
           if (!left[r]) continue;
           int grow = 0;
           for (int c = 0; c < C; c++) grow += sup[r][c] && !U[c];
-          if (grow < bgrow) { bgrow = grow; best = r; }
+          // ties (typically 0: the seed already reads every input): the widest row, so that
+          // rows of similar weight share a group (decode: dense rows of lost data vs sparse ones)
+          if (grow < bgrow || (o.cluster_wide && grow == bgrow && w[r] > w[best])) { bgrow = grow; best = r; }
         }
         g.rows.push_back(best);
         left[best] = 0;
@@ -557,6 +562,88 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   }
   int qmax = 1;
   for (auto &sg : stages) qmax = std::max(qmax, (int)sg.blocks.size());
+  // ---- rows -> team ranks: rank rk computes rows [m*rk/T, m*(rk+1)/T) of its group's row list and
+  // transposes blocks [n*rk/T, n*(rk+1)/T) of every stage; the ranks meet at a barrier per stage, so
+  // reorder the rows to balance (XOR work + transposes) per rank (longest-processing-time greedy).
+  // (Option, off by default: measured slower for decode and encode.)
+  if (o.balance_ranks && o.team >= 2 && !(o.ws && o.layout >= 1)) {
+    const int TT = o.team;
+    for (size_t g = 0; g < groups.size(); g++) {
+      Group &G = groups[g];
+      const int mall = (int)G.rows.size();
+      if (mall < 2) continue;
+      std::vector<double> load(TT, 0.0);
+      std::vector<int> room(TT);
+      for (int rk = 0; rk < TT; rk++) {
+        room[rk] = mall * (rk + 1) / TT - mall * rk / TT;
+        for (int si : gstages[g]) {
+          const int nb = (int)stages[si].blocks.size();
+          load[rk] += 44.0 * (nb * (rk + 1) / TT - nb * rk / TT);  // a transpose ~ 44 XOR2 of issue
+        }
+        load[rk] += 44.0 * room[rk];  // output transposes
+      }
+      std::vector<std::pair<double, int>> cost;
+      for (int r : G.rows) {
+        long ones = 0;
+        for (int c : G.cols)
+          if (const uint32_t cf = p.coef(r, c)) {
+            uint32_t br[16];
+            coef_rows_w(W, cf, br);
+            for (int b = 0; b < W; b++) ones += __builtin_popcount(br[b]);
+          }
+        cost.push_back({0.55 * (double)ones, r});  // ~ XOR2 after CSE
+      }
+      double lo = 1e300, hi = 0;
+      for (auto &cr : cost) lo = std::min(lo, cr.first), hi = std::max(hi, cr.first);
+      if (hi <= 1.1 * lo) continue;  // rows alike: keep the order
+      std::stable_sort(cost.begin(), cost.end(), [](const std::pair<double, int> &a, const std::pair<double, int> &b) {
+        return a.first > b.first;
+      });
+      std::vector<std::vector<int>> lists(TT);
+      for (auto &cr : cost) {
+        int best = -1;
+        for (int rk = 0; rk < TT; rk++)
+          if ((int)lists[rk].size() < room[rk] && (best < 0 || load[rk] < load[best])) best = rk;
+        lists[best].push_back(cr.second);
+        load[best] += cr.first;
+      }
+      // pairwise swaps between ranks while they lower the larger of the two loads (the fixed row
+      // counts per rank keep LPT alone from balancing rows of similar cost)
+      std::map<int, double> rc;
+      for (auto &cr : cost) rc[cr.second] = cr.first;
+      for (int it = 0; it < 64; it++) {
+        double gain = 0;
+        int ba = -1, bb = -1, bi = -1, bj = -1;
+        for (int a = 0; a < TT; a++)
+          for (int b = 0; b < TT; b++) {
+            if (load[a] <= load[b]) continue;
+            for (size_t i = 0; i < lists[a].size(); i++)
+              for (size_t j = 0; j < lists[b].size(); j++) {
+                const double d = rc[lists[a][i]] - rc[lists[b][j]];
+                if (d <= 0) continue;
+                const double nm = std::max(load[a] - d, load[b] + d), g0 = load[a] - nm;
+                if (g0 > gain) gain = g0, ba = a, bb = b, bi = (int)i, bj = (int)j;
+              }
+          }
+        if (ba < 0) break;
+        const double d = rc[lists[ba][bi]] - rc[lists[bb][bj]];
+        std::swap(lists[ba][bi], lists[bb][bj]);
+        load[ba] -= d;
+        load[bb] += d;
+      }
+      if (getenv("PMRC_DEBUG_BAL"))
+        for (int rk = 0; rk < TT; rk++) {
+          fprintf(stderr, "group %zu rank %d load %.0f rows", g, rk, load[rk]);
+          for (int r : lists[rk]) fprintf(stderr, " %d:%.0f", r, rc[r]);
+          fprintf(stderr, "\n");
+        }
+      G.rows.clear();
+      for (auto &l : lists) {
+        std::sort(l.begin(), l.end());
+        G.rows.insert(G.rows.end(), l.begin(), l.end());
+      }
+    }
+  }
   // L2 policy: a loaded block keeps normal priority if a later stage of the tile loads it again
   {
     std::map<std::pair<int, int>, std::pair<int, int>> last;  // block -> (stage, index) of last read

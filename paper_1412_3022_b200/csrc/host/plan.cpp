@@ -97,7 +97,8 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     (void)generate_source(p, oo, g0);
     const int G = std::max(1, g0.groups), sms = 148;
     oo.layout = (G <= sms && (sms % G) * 10 <= sms) ? 1 : 0;
-    if (oo.layout == 1 && g0.group_cost_ratio > 1.2) oo.layout = 2;  // unequal groups: apportion CTAs
+    // unequal groups: apportion CTAs by cost (layout 2), unless the dynamic schedule balances them
+    if (oo.layout == 1 && g0.group_cost_ratio > 1.2 && oo.dyn <= 0) oo.layout = 2;
   }
   if (oo.ws) {  // ws_prod producers + 2 consumers per team, <= 4 teams (4 named barriers each), 2 buffers
     oo.team = std::max(1, oo.ws_prod) + 2;

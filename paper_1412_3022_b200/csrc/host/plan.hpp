@@ -59,6 +59,12 @@ struct GenOptions {
   int layout = -1;          // 0: every CTA walks all groups; 1: group-specialised CTAs; 2: same, CTAs
                             // apportioned by group cost; -1: auto
   int grid_ctas = 148;      // layout 2: CTAs the apportionment table is made for (one per SM)
+  bool balance_ranks = false; // reorder a group's rows to balance estimated work per team rank
+                             // (measured: decode 0.651 -> 0.663 ms, encode 0.528 -> 0.532: off)
+  bool cluster_wide = false; // clustering ties -> the widest row (dense and sparse decode rows in
+                             // different groups; measured 0.651 -> 0.734 ms: the groups' fronts drift
+                             // apart and the shared inputs are read from DRAM twice)
+  bool even_groups = false; // clustered plans: equal group sizes instead of max_rows-sized groups
   bool auto_wide = true;    // resolve_options: 16-row groups on 4-warp teams for wide multi-stage plans
   int cse_restarts = 1;     // CSE runs per network (seeded near-tie randomisation), keep the cheapest
   bool sched = false;       // register-pressure-aware temp order (emit_slp_sched) instead of CSE order

@@ -226,6 +226,7 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "cta_sync") c->gen.cta_sync = v;
         if (key == "dyn") c->gen.dyn = v;
         if (key == "even_groups") c->gen.even_groups = v != 0;
+        if (key == "tr_balance") c->gen.tr_balance = v != 0;
         if (key == "cluster_wide") c->gen.cluster_wide = v != 0;
         if (key == "balance_ranks") c->gen.balance_ranks = v != 0;
         if (key == "ld_hint") c->gen.ld_hint = v;

@@ -1,3 +1,4 @@
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 // Generator of the bitsliced sm_100a region-linear-combination kernels.
@@ -562,6 +563,79 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
   }
   int qmax = 1;
   for (auto &sg : stages) qmax = std::max(qmax, (int)sg.blocks.size());
+  // ---- per-stage split of the loaded blocks over the team ranks: rank rk loads (cp.async) and
+  // transposes blocks [tsplit[si][rk], tsplit[si][rk + 1]) of stage si (a warp can only wait for its
+  // own copies, so loads and transposes split alike).  Default: equal shares.  tr_balance: shares
+  // that equalise each rank's (XOR network + transposes) per item, from the networks' LOP3 counts,
+  // since the ranks meet at a barrier every stage (decode rows differ 4x in XOR work).
+  std::vector<std::vector<int>> tsplit(stages.size());
+  {
+    const int TT = std::max(1, o.team);
+    const bool ws_on = o.ws && o.layout >= 1 && TT >= 2;
+    const int NPk = ws_on ? std::max(1, std::min(TT - 1, o.ws_prod)) : 0;
+    for (size_t si = 0; si < stages.size(); si++) {
+      const int n = (int)stages[si].blocks.size(), parts = ws_on ? NPk : TT;
+      for (int rk = 0; rk <= parts; rk++) tsplit[si].push_back(n * rk / parts);
+    }
+    if (o.tr_balance && TT >= 2 && !ws_on) {
+      const int sub_in = o.net_in > 0 ? (W == 16 ? (o.net_in + 1) / 2 : o.net_in) : 0;
+      for (size_t g = 0; g < groups.size(); g++) {
+        const Group &G = groups[g];
+        const int mall = (int)G.rows.size();
+        std::vector<double> net(TT, 0.0);
+        int n_in = 0;
+        for (int si : gstages[g]) n_in += (int)stages[si].blocks.size();
+        for (int rk = 0; rk < TT; rk++) {
+          const int r0 = mall * rk / TT, m = mall * (rk + 1) / TT - r0;
+          net[rk] += 24.0 * m;  // output transposes
+          for (int si : gstages[g]) {
+            const Stage &sg = stages[si];
+            std::vector<std::vector<int>> rows(W * m);
+            for (int r = 0; r < m; r++)
+              for (size_t ci = 0; ci < sg.cols.size(); ci++) {
+                const uint32_t cf = p.coef(G.rows[r0 + r], sg.cols[ci]);
+                if (!cf) continue;
+                uint32_t br[16];
+                coef_rows_w(W, cf, br);
+                for (int b = 0; b < W; b++)
+                  for (int bp = 0; bp < W; bp++)
+                    if ((br[b] >> bp) & 1) rows[r * W + b].push_back((int)ci * W + bp);
+              }
+            const int ncols = (int)sg.cols.size();
+            int sub = sub_in > 0 ? sub_in : ncols;
+            if (o.net_even && sub < ncols) {
+              const int nsub = (ncols + sub - 1) / sub;
+              sub = (ncols + nsub - 1) / nsub;
+            }
+            for (int c0 = 0; c0 < ncols; c0 += sub) {
+              const int c1 = std::min(ncols, c0 + sub);
+              std::vector<std::vector<int>> sr(rows.size());
+              for (size_t r = 0; r < rows.size(); r++)
+                for (int x : rows[r])
+                  if (x >= W * c0 && x < W * c1) sr[r].push_back(x - W * c0);
+              net[rk] += (double)make_slp(W * (c1 - c0), sr, o.cse, o.cse_restarts).lop3() + 0.5 * W * m;
+            }
+          }
+        }
+        // water-fill the group's n_in input transposes (24 LOP3-equivalents each) over the ranks
+        std::vector<int> x(TT, 0);
+        for (int k = 0; k < n_in; k++) {
+          int best = 0;
+          for (int rk = 1; rk < TT; rk++)
+            if (net[rk] + 24.0 * x[rk] < net[best] + 24.0 * x[best]) best = rk;
+          x[best]++;
+        }
+        // per stage: cumulative rounding of the shares x[rk] / n_in
+        std::vector<double> cum(TT + 1, 0.0);
+        for (int rk = 0; rk < TT; rk++) cum[rk + 1] = cum[rk] + x[rk];
+        for (int si : gstages[g]) {
+          const int n = (int)stages[si].blocks.size();
+          for (int rk = 0; rk <= TT; rk++)
+            tsplit[si][rk] = n_in ? (int)std::lround(cum[rk] * n / n_in) : n * rk / TT;
+        }
+      }
+    }
+  }
   // ---- rows -> team ranks: rank rk computes rows [m*rk/T, m*(rk+1)/T) of its group's row list and
   // transposes blocks [n*rk/T, n*(rk+1)/T) of every stage; the ranks meet at a barrier per stage, so
   // reorder the rows to balance (XOR work + transposes) per rank (longest-processing-time greedy).
@@ -790,7 +864,7 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
     o2 << ind << "  const u32 dst = sbuf + (" << bb << ") * (PM_QMAX * " << CB << "u) + lane * 16u;\n";
     o2 << ind << "  switch (rank) {\n";
     for (int rk = 0; rk < (WS ? NP : T); rk++) {
-      const int lo = WS ? n * rk / NP : n * rk / T, hi = WS ? n * (rk + 1) / NP : n * (rk + 1) / T;
+      const int lo = tsplit[sid][rk], hi = tsplit[sid][rk + 1];
       o2 << ind << "  case " << rk << ": {\n";
       std::map<int, bool> slots;
       for (int i = lo; i < hi; i++) slots[sg.blocks[i].first] = true;
@@ -885,7 +959,7 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
             // consumers released the other buffer (EMPTY) before loading the successor stage
             s << "          pm_cp_wait<0>();\n";
             if (!(o.debug & 1))
-              s << "          pm_transpose_in(buf + lane * 16u, " << nblk * rk / NP << "u, " << nblk * (rk + 1) / NP << "u);\n";
+              s << "          pm_transpose_in(buf + lane * 16u, " << tsplit[si][rk] << "u, " << tsplit[si][rk + 1] << "u);\n";
             s << "          pm_team_arrive(4u * team + pb, PM_T * 32u);\n";
             s << "          if (kk != 0u" << (sj ? " || true" : "") << ") pm_team_sync(4u * team + 2u + (pb ^ 1u), PM_T * 32u);\n";
             prefetch(g, sj);
@@ -899,7 +973,7 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
         s << "          pm_cp_wait<" << (D - 1) << ">();\n";
         s << "          const u32 buf = sbuf + pb * (PM_QMAX * " << CB << "u);\n";
         if (!(o.debug & 1))  // debug bit 0: skip the input transposes (timing experiments only: wrong results)
-          s << "          pm_transpose_in(buf + lane * 16u, " << nblk * rk / T << "u, " << nblk * (rk + 1) / T << "u);\n";
+          s << "          pm_transpose_in(buf + lane * 16u, " << tsplit[si][rk] << "u, " << tsplit[si][rk + 1] << "u);\n";
         s << "          const u32 pl = buf + lane * 16u;\n";
         }
         // the team barrier + the prefetch of the successor stage into the other buffer; emitted
@@ -990,7 +1064,7 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
           st.naive_lop3 += naive_lop3(rows);
           // sub-networks whose inputs are all plain blocks this warp transposed itself run before
           // the team barrier (their planes are already in place), the rest after it
-          const int own_lo = nblk * rk / T, own_hi = nblk * (rk + 1) / T;
+          const int own_lo = tsplit[si][rk], own_hi = tsplit[si][rk + 1];
           std::vector<int> order_pre, order_post;
           for (size_t si2 = 0; si2 < subs.size(); si2++) {
             bool own = T > 1 && o.own_first && !WS;
@@ -1179,6 +1253,12 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
     s << "  const u32 c0 = (u32)((lo + wg - 1u) / wg), c1 = (u32)((hi + wg - 1u) / wg);\n";
     s << "  g = gs;\n  pb = 0u;\n";
   } else {
+    if (DYN && o.dyn >= 2 && groups.size() > 1) {
+      // steal mode runs on the full grid: the gridDim.x % G CTAs beyond G x spg start as visitors
+      s << "  const u32 spg = gridDim.x / " << groups.size() << "u;\n";
+      s << "  u32 g = blockIdx.x / spg, r = blockIdx.x - g * spg;\n";
+      s << "  if (blockIdx.x >= " << groups.size() << "u * spg) { g = blockIdx.x - " << groups.size() << "u * spg; r = spg; }\n";
+    } else
     s << "  const u32 spg = gridDim.x / " << groups.size() << "u, g = blockIdx.x / spg, r = blockIdx.x - g * spg;\n";
     s << "  const u32 total = stripes * chunks;\n";
     s << "  const u32 c0 = (u32)((u64)total * r / spg), c1 = (u32)((u64)total * (r + 1u) / spg);\n";
@@ -1205,7 +1285,7 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
         // also keeps the team's last buffer from being overwritten while a rank still reads it)
         s << "    pb = 0u;\n";
         s << "    u32 tau = r * teams + team;\n";
-        s << "    if (hop != 0u) {\n";
+        s << "    if (hop != 0u || r >= spg) {\n";
         // (own slots, double-buffered by hop: a rank may still read the loop slots or the previous
         // hop's slot when rank 0 gets here)
         s << "      const u32 hs = 2u * teams + 2u * team + (hop & 1u);\n";

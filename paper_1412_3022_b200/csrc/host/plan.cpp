@@ -263,6 +263,7 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
       return PMRC_ENOMEM;
     }
     k.dyn_on = true;
+    k.dyn_full = k.source.find("for (u32 hop = 0;") != std::string::npos;
   }
   return PMRC_OK;
 }
@@ -273,6 +274,7 @@ void free_kernel(Kernel &k) {
   if (k.dyn) cudaFree(k.dyn);
   k.dyn = nullptr;
   k.dyn_on = false;
+  k.dyn_full = false;
   if (k.module && drv().ok) drv().ModuleUnload((CUmodule)k.module);
   k.module = nullptr;
   k.function = nullptr;
@@ -309,7 +311,8 @@ int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides
       const uint64_t G = (uint64_t)k.n_groups;
       uint64_t spg = std::max<uint64_t>(1, grid / G);
       spg = std::min<uint64_t>(spg, (uint64_t)ns * chunks);
-      grid = G * spg;
+      // (the stealing schedule also uses the grid % G CTAs beyond G x spg, as visitors)
+      grid = k.dyn_full && grid >= G ? std::min<uint64_t>(grid, G * spg + G - 1) : G * spg;
     } else {
       grid = std::min<uint64_t>(grid, (uint64_t)ns * chunks);
       grid = std::max<uint64_t>(grid, 1);

@@ -59,6 +59,8 @@ struct GenOptions {
   int layout = -1;          // 0: every CTA walks all groups; 1: group-specialised CTAs; 2: same, CTAs
                             // apportioned by group cost; -1: auto
   int grid_ctas = 148;      // layout 2: CTAs the apportionment table is made for (one per SM)
+  bool tr_balance = false;   // split a stage's loads + transposes over team ranks by network cost
+                             // (measured: config-4 decode 0.647 -> 0.680 ms: off)
   bool balance_ranks = false; // reorder a group's rows to balance estimated work per team rank
                              // (measured: decode 0.651 -> 0.663 ms, encode 0.528 -> 0.532: off)
   bool cluster_wide = false; // clustering ties -> the widest row (dense and sparse decode rows in
@@ -116,6 +118,7 @@ struct Kernel {
   size_t pace_entries = 0;
   void *dyn = nullptr;              // layout 1 dynamic schedule: kDynSlots x n_groups x 2 u32 counters
   bool dyn_on = false;
+  bool dyn_full = false;            // stealing schedule: launched on the full grid (not G x spg)
   mutable uint32_t epoch = 0;       // launch epoch (counters carry it, so they never need a reset)
   size_t smem = 0;
   int blocks_per_sm = 1;

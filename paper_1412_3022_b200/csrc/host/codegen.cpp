@@ -916,9 +916,12 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
   const int teams = TPB / 32 / T;
   // dynamic chunk schedule (layout 1): teams take their next chunk from a per-group counter
   const bool DYN = o.dyn > 0 && o.layout == 1 && !WS && NB == 2 && o.pace_lag == 0 && o.cta_sync == 0;
+  const bool HYB = DYN && o.dyn >= 2 && groups.size() > 1 && o.dyn_static > 0;  // static ranges + pool
+  // layout 0 with dynamic tiles: a CTA takes its next tile of teams x chunk_loop chunks from a counter
+  const bool DYN0 = o.dyn > 0 && o.layout == 0 && o.sync_groups;
   s << "extern \"C\" __global__ void __launch_bounds__(" << TPB << ", 1) pmrc_kernel(const __grid_constant__ Slots R, "
        "const u64 S, const u32 stripes, const u32 chunks, u64 *__restrict__ pace, const u32 epoch"
-    << (DYN ? ", u32 *__restrict__ dyn" : "") << ") {\n";
+    << ((DYN || DYN0) ? ", u32 *__restrict__ dyn" : "") << ") {\n";
   s << "  extern __shared__ __align__(1024) unsigned char pm_smem[];\n";
   s << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, team = warp / PM_T, rank = warp - team * PM_T;\n";
   s << "  u32 dv_m, dv_s1, dv_s2;\n  pm_udiv_setup(chunks, dv_m, dv_s1, dv_s2);\n";
@@ -1171,8 +1174,17 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
   // chunks are split evenly over the teams, so the last (short) step costs ~1 chunk, not a tile.
   s << "  const u32 teams = " << teams << "u, per = " << teams << "u * " << M << "u;\n";
   s << "  const u32 total = stripes * chunks;\n";
+  if (DYN0) {
+    // tiles of `per` chunks: CTA b starts with tile b, then takes gridDim.x + atomicAdd (thread 0,
+    // one tile ahead, published through shared memory behind a CTA barrier)
+    s << "  const u32 ntiles = (total + per - 1u) / per;\n";
+    s << "  __shared__ u32 pm_nt[2];\n";
+    s << "  u32 tile = blockIdx.x, nxt_tile = threadIdx.x == 0u ? gridDim.x + atomicAdd(dyn, 1u) : 0u;\n";
+    s << "  const u32 c0 = min(total, tile * per), c1 = min(total, c0 + per);\n";
+  } else {
   s << "  const u32 per_cta = (total + gridDim.x - 1u) / gridDim.x;\n";
   s << "  const u32 c0 = blockIdx.x * per_cta, c1 = min(total, c0 + per_cta);\n";
+  }
   s << "  const u32 sbuf = pm_saddr(pm_smem) + team * (" << NB << "u * PM_QMAX * " << CB << "u);\n";
   s << "  const u64 pol_ef = pm_policy_ef(), pol_en = pm_policy_en(), pol_el = pm_policy_el();\n";
   s << "  u32 pb = 0u;\n";
@@ -1183,12 +1195,25 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
     s << "  }\n";
   }
   s << "  pm_cp_commit();\n";
+  if (DYN0) {
+    s << "  for (u32 it = 0; tile < ntiles; it++) {\n";
+    s << "    const u32 base = tile * per;\n";
+    s << "    const u32 n = min(per, total - base), mt = (n + teams - 1u) / teams;\n";
+    s << "    const u32 tb = base + team * mt;\n";
+    s << "    const u32 cnt = team * mt < n ? min(mt, n - team * mt) : 0u;\n";
+    s << "    if (threadIdx.x == 0u) { pm_nt[it & 1u] = nxt_tile; nxt_tile = gridDim.x + atomicAdd(dyn, 1u); }\n";
+    s << "    __syncthreads();\n";
+    s << "    const u32 ntile = pm_nt[it & 1u];\n";
+    s << "    const u32 nbase = ntile * per;\n";
+    s << "    const u32 nn = ntile < ntiles ? min(per, total - nbase) : 0u, nmt = (nn + teams - 1u) / teams;\n";
+  } else {
   s << "  for (u32 base = c0; base < c1; base += per) {\n";
   s << "    const u32 n = min(per, c1 - base), mt = (n + teams - 1u) / teams;\n";
   s << "    const u32 tb = base + team * mt;\n";
   s << "    const u32 cnt = team * mt < n ? min(mt, n - team * mt) : 0u;\n";
   s << "    const u32 nbase = base + per;\n";
   s << "    const u32 nn = nbase < c1 ? min(per, c1 - nbase) : 0u, nmt = (nn + teams - 1u) / teams;\n";
+  }
   for (size_t g = 0; g < groups.size(); g++) {
     // successor group with stages (for the prefetch after this group's last stage at m = M-1)
     int next_g = -1;
@@ -1226,6 +1251,11 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
     });
     s << "    }\n";
   }
+  if (DYN0) {
+    s << "    tile = ntile;\n  }\n";
+    s << "  if (threadIdx.x == 0u) { __threadfence(); if (atomicAdd(dyn + 1, 1u) == gridDim.x - 1u) "
+         "{ atomicExch(dyn, 0u); atomicExch(dyn + 1, 0u); } }\n}\n";
+  } else
   s << "  }\n}\n";
   } else {
   // layout 1 (group-specialised CTAs): CTA b computes group g = b / spg only, over chunk range
@@ -1261,6 +1291,12 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
     } else
     s << "  const u32 spg = gridDim.x / " << groups.size() << "u, g = blockIdx.x / spg, r = blockIdx.x - g * spg;\n";
     s << "  const u32 total = stripes * chunks;\n";
+    if (HYB) {
+      // hybrid: static equal ranges over the first dyn_static / 1000 of the chunks, the rest is a pool
+      // handed out by the per-group counters (the slow-TPC tail is absorbed there)
+      s << "  const u32 P0 = (u32)((u64)total * " << o.dyn_static << "u / 1000u);\n";
+      s << "  const u32 c0 = (u32)((u64)P0 * r / spg), c1 = (u32)((u64)P0 * (r + 1u) / spg);\n";
+    } else
     s << "  const u32 c0 = (u32)((u64)total * r / spg), c1 = (u32)((u64)total * (r + 1u) / spg);\n";
     if (DYN) s << "  __shared__ u32 pm_nx[" << 4 * teams << "];\n";
   }
@@ -1280,7 +1316,20 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
       // item and passed to the team through shared memory (read after the item's first barrier)
       s << "    const u32 NT = spg * teams;\n";
       s << "    u32 *const dctr = dyn + 2u * " << g << "u;\n";
-      if (STEAL) {
+      if (HYB) {
+        // own group: the static range first (sn = next static chunk), then the pool; other groups
+        // (hop != 0) and the visitor CTAs: the pool only.  First chunk: static, else from the
+        // counter, broadcast through the team barrier (slots double-buffered by hop)
+        s << "    pb = 0u;\n";
+        s << "    const u32 cl = hop == 0u ? c1 : 0u;\n";
+        s << "    u32 sn = c0 + team, tau;\n";
+        s << "    if (sn < cl) { tau = sn; sn += teams; } else {\n";
+        s << "      const u32 hs = 2u * teams + 2u * team + (hop & 1u);\n";
+        s << "      if (rank == 0u && lane == 0u) pm_nx[hs] = P0 + atomicAdd(dctr, 1u);\n";
+        s << "      " << (T > 1 ? "pm_team_sync(1u + team, PM_T * 32u);" : "__syncwarp();") << "\n";
+        s << "      tau = pm_nx[hs];\n";
+        s << "    }\n";
+      } else if (STEAL) {
         // a visiting team starts from the counter too (broadcast through the team barrier, which
         // also keeps the team's last buffer from being overwritten while a rank still reads it)
         s << "    pb = 0u;\n";
@@ -1326,9 +1375,11 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
     } else if (DYN) {
       // rank 0 takes its counter value one item ahead (the atomic's L2 round trip overlaps a whole
       // item): item kk publishes the value taken during item kk - 1
-      s << "    u32 nxt = (rank == 0u && lane == 0u) ? NT + atomicAdd(dctr, 1u) : 0u;\n";
+      const std::string take = HYB ? "(sn < cl ? (sn += teams) - teams : P0 + atomicAdd(dctr, 1u))"
+                                   : "NT + atomicAdd(dctr, 1u)";
+      s << "    u32 nxt = (rank == 0u && lane == 0u) ? " << take << " : 0u;\n";
       s << "    for (u32 gi = tau, kk = 0; gi < total; kk++) {\n";
-      s << "      if (rank == 0u && lane == 0u) { pm_nx[2u * team + (kk & 1u)] = nxt; nxt = NT + atomicAdd(dctr, 1u); }\n";
+      s << "      if (rank == 0u && lane == 0u) { pm_nx[2u * team + (kk & 1u)] = nxt; nxt = " << take << "; }\n";
     } else
     s << "    for (u32 gi = c0 + team, kk = 0; gi < c1; gi += teams, kk++) {\n";
     const int pace_lag = o.layout == 1 ? o.pace_lag : 0;  // pacing assumes aligned (layout 1) ranges

@@ -50,6 +50,7 @@ struct GenOptions {
   int dyn = -1;             // layout 1: dynamic chunk schedule (per-group counters) instead of static
                             // ranges; 2: teams then help the other groups (-1 auto: 2 for clustered
                             // plans, i.e. decode, else 0)
+  int dyn_static = 0;        // dyn >= 2: per mille of the chunks in static ranges (the rest: the counters)
   int cta_sync = 0;         // layout 1: all teams of a CTA start every item together (CTA barrier):
                             // the teams then fetch the same instructions at about the same time
   int chunk_loop = 24;      // chunks per team per group (loop: instruction reuse)

@@ -460,6 +460,7 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     by_support[sup].push_back(r);
   }
   std::vector<Group> groups;
+  for (auto &kv : by_support) st.max_support_rows = std::max(st.max_support_rows, (int)kv.second.size());
   for (auto &kv : by_support)
     for (size_t i = 0; i < kv.second.size(); i += o.max_rows) {
       Group g;

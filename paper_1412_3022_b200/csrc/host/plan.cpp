@@ -73,6 +73,15 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
       oo.max_rows = 16;
       oo.team = 4;
       if (oo.warps <= 0) oo.warps = 16;
+    } else if (o.auto_wide16 && p.w != 16 && !w0.clustered && w0.max_support_rows >= 16 && w0.groups > 16 &&
+               oo.team == 2 && oo.max_rows == 8 && oo.layout < 0) {
+      // many groups whose supports have >= 16 rows (k = 16 encode: 30 groups of 8 rows, two per
+      // support): pairs of them as 16-row groups on 4-warp teams halve the input transposes; layout 0
+      // (measured: MSR k=16 869 -> 901 GB/s; layout 1 with these groups 606)
+      oo.max_rows = 16;
+      oo.team = 4;
+      oo.layout = 0;
+      if (oo.warps <= 0) oo.warps = 16;
     }
   }
   if (oo.dyn < 0) {

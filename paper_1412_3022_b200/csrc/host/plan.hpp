@@ -68,6 +68,8 @@ struct GenOptions {
                              // different groups; measured 0.651 -> 0.734 ms: the groups' fronts drift
                              // apart and the shared inputs are read from DRAM twice)
   bool even_groups = false; // clustered plans: equal group sizes instead of max_rows-sized groups
+  bool auto_wide16 = true;   // resolve_options: 16-row groups on 4-warp teams, layout 0, for many
+                             // groups whose supports have >= 16 rows (k = 16 encode)
   bool auto_wide = true;    // resolve_options: 16-row groups on 4-warp teams for wide multi-stage plans
   int cse_restarts = 1;     // CSE runs per network (seeded near-tie randomisation), keep the cheapest
   bool sched = false;       // register-pressure-aware temp order (emit_slp_sched) instead of CSE order
@@ -96,6 +98,7 @@ struct GenStats {
   long loads = 0;        // 16-B vector loads per lane per item sum
   int smem_per_warp = 0; // bytes of shared memory (transposed input planes) per warp
   int max_stages = 0;    // most shared-memory stages of any group
+  int max_support_rows = 0;  // most output rows sharing one support (before the max_rows split)
   bool clustered = false;  // rows had distinct supports and were clustered greedily
   double group_cost_ratio = 1;  // max / min estimated group cost (loaded blocks + outputs)
 };

@@ -41,6 +41,7 @@ class ClockSampler:
 
     def __init__(self, dev_index):
         self.samples, self.reasons, self.stop_flag = [], set(), False
+        self.interval = float(os.environ.get("PMRC_CLOCK_INTERVAL", "0.005"))  # seconds between NVML samples
         self.max_mhz = None
         try:
             import pynvml
@@ -69,7 +70,7 @@ class ClockSampler:
                         self.reasons.add(n_)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(self.interval)
 
     def __enter__(self):
         if self.nv:

@@ -93,7 +93,7 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     if (p1.layout < 0) p1.layout = 0;
     GenStats w1;
     (void)generate_source(p, p1, w1);
-    oo.dyn = w1.clustered ? 2 : 0;
+    if (w1.clustered) oo.dyn = 2;
   }
   if (p.w == 16) {  // 16 planes per row: groups of 4 rows (2 per warp), stages of <= 8 blocks of 2 KiB
     if (oo.team == 2 && oo.max_rows == 8) oo.max_rows = 4;      // measured: k=8 0.54 -> 0.74 TB/s
@@ -108,6 +108,14 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     oo.layout = (G <= sms && (sms % G) * 10 <= sms) ? 1 : 0;
     // unequal groups: apportion CTAs by cost (layout 2), unless the dynamic schedule balances them
     if (oo.layout == 1 && g0.group_cost_ratio > 1.2 && oo.dyn <= 0) oo.layout = 2;
+  }
+  if (oo.dyn < 0) {
+    // group-specialised plans whose groups leave >= 4 SMs without a group (G x spg < 148): the
+    // stealing schedule puts those SMs to work as visitors (GF(2^16) k=8 encode, 14 groups:
+    // 767 -> 822 GB/s); with <= 3 idle SMs static ranges measured better (GF(2^8) k=8: 7 groups)
+    GenStats g2;
+    (void)generate_source(p, oo, g2);
+    oo.dyn = (oo.layout == 1 && g2.groups > 1 && 148 % g2.groups >= 4) ? 2 : 0;
   }
   if (oo.ws) {  // ws_prod producers + 2 consumers per team, <= 4 teams (4 named barriers each), 2 buffers
     oo.team = std::max(1, oo.ws_prod) + 2;

@@ -564,3 +564,31 @@ def test_repair_gf16():
         assert e.value.rc == pm.PMRC_ESINGULAR
     finally:
         pm.pmrc_destroy(code)
+
+
+def test_decode_dynamic_schedule_concurrent_streams_and_tiny():
+    # decode plans take chunks from per-group counters (a ring of counter slots, one per launch):
+    # the same plan launched back to back on two streams, more launches than a slot ring's worth of
+    # in-flight work, and launches with fewer chunks than teams must all stay bit-exact
+    k, n = 8, 16
+    ids = [0, 1, 4, 5, 9, 12, 14, 15]
+    for S, stripes in ((64 * 1024, 6), (16, 1), (1024 + 16, 3)):
+        st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=21)
+        try:
+            st.encode()
+            assert "atomicAdd(dctr" in pm.pmrc_plan_source(st.code, 0, 0, ids)
+            streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+            outs = [st.data.clone() for _ in range(4)]
+            for o in outs:
+                for i in (2, 3, 6, 7):
+                    o[:, i * st.alpha:(i + 1) * st.alpha] = 0xCC
+            torch.cuda.synchronize()
+            for rep in range(80):       # > 64 launches of one plan, alternating streams
+                o = outs[rep % 4]
+                s = streams[rep % 2]
+                pm.pmrc_decode(st.code, ids, [st.piece(i) for i in ids], o.data_ptr(), S, stripes, s.cuda_stream)
+            torch.cuda.synchronize()
+            for o in outs:
+                assert torch.equal(o, st.data), (S, stripes)
+        finally:
+            st.close()

@@ -21,7 +21,8 @@ MATRIX_PSI, MATRIX_G, MATRIX_GSYS, MATRIX_GPP, MATRIX_LAMBDA, MATRIX_GTINV = 0, 
 EXPORTS = ["pmrc_create", "pmrc_destroy", "pmrc_info", "pmrc_matrix", "pmrc_layout", "pmrc_encode",
            "pmrc_encode_host", "pmrc_decode", "pmrc_repair", "pmrc_repair_project", "pmrc_repair_combine",
            "pmrc_read_cost", "pmrc_launch_count", "pmrc_strerror", "pmrc_last_error", "pmrc_precompile",
-           "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source", "pmrc_plan_stats", "pmrc_apply", "pmrc_apply_stats", "pmrc_set_max_ctas"]
+           "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source", "pmrc_plan_stats", "pmrc_apply", "pmrc_apply_stats", "pmrc_set_max_ctas",
+           "pmrc_set_independent_launches"]
 
 
 class PmrcError(RuntimeError):
@@ -87,6 +88,7 @@ def lib():
             "pmrc_apply": ([P, P, I, I, P, Z, P, Z, Z, Z, P], I),
             "pmrc_apply_stats": ([P, P, I, I, ctypes.POINTER(pmrc_plan_stats_t)], I),
             "pmrc_set_max_ctas": ([P, I], I),
+            "pmrc_set_independent_launches": ([P, I], I),
             "pmrc_strerror": ([I], ctypes.c_char_p),
             "pmrc_last_error": ([], ctypes.c_char_p),
         }
@@ -229,6 +231,11 @@ def pmrc_set_max_ctas(code, max_ctas):
     _check(lib().pmrc_set_max_ctas(code, max_ctas), "pmrc_set_max_ctas")
 
 
+def pmrc_set_independent_launches(code, on):
+    """Declare consecutive launches of this handle independent (programmatic dependent launch)."""
+    _check(lib().pmrc_set_independent_launches(code, int(on)), "pmrc_set_independent_launches")
+
+
 def pmrc_apply_stats(code, A):
     """Per-stripe work of the pmrc_apply plan for matrix A."""
     import numpy as np
@@ -246,19 +253,23 @@ def pmrc_plan_stats(code, op, lost_id=0, ids=()):
     return {f: getattr(st, f) for f, _ in pmrc_plan_stats_t._fields_}
 
 
-def prepare_plans(kind, k, d, n, patterns, threads=None):
+def prepare_plans(kind, k, d, n, patterns, threads=None, independent=False):
     """Pre-compile the decode / repair plans of many failure patterns in parallel (NVRTC runs
     outside the GIL; each worker thread uses its own handle, and the cubins land in the shared
     in-tree kernel cache, keyed by source), so that the first pmrc_decode / pmrc_repair of each
     pattern only loads a cubin.  patterns: iterable of ("decode", survivor_ids) or
     ("repair", lost_id, helper_ids).  Returns the list of (pattern, rc) (rc = PMRC_ESINGULAR for
-    singular helper sets)."""
+    singular helper sets).  independent=True prepares the kernels a handle uses after
+    pmrc_set_independent_launches(code, 1)."""
     import os
     from concurrent.futures import ThreadPoolExecutor
     pats = list(patterns)
     threads = threads or min(len(pats), os.cpu_count() or 4) or 1
     handles = [pmrc_create(kind, k, d, n) for _ in range(threads)]
     try:
+        if independent:
+            for h in handles:
+                pmrc_set_independent_launches(h, 1)
         def work(i):
             h = handles[i % threads]
             out = []

@@ -79,14 +79,24 @@ PRECOMPILE_DECODE = [(0, 8, 14, 16, 16, 0, 0, (0, 1, 4, 5, 9, 12, 14, 15)),
                      (0, 8, 14, 16, 16, 0, 0, tuple(range(8, 16))),
                      (0, 8, 14, 16, 16, 1, 15, (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 11, 12, 13, 14)),
                      (0, 8, 14, 16, 16, 1, 3, (0, 1, 2, 4, 5, 6, 7, 8, 9, 10, 12, 13, 14, 15))]
+# + the independent-launch (programmatic dependent launch) plans of
+# test_independent_launches_per_stripe_repair_and_decode: (..., independent=1)
+_IND_REP = [(6, (0, 1, 2, 3, 4, 5, 7, 8, 9, 10, 11, 13, 14, 15)), (15, (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 11, 12, 13, 14)),
+            (8, (0, 1, 2, 3, 4, 5, 6, 9, 10, 11, 12, 13, 14, 15)), (3, (0, 1, 2, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14)),
+            (12, (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 13, 14)), (0, (1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 15))]
+_IND_DEC = [(0, 1, 4, 5, 9, 12, 14, 15), tuple(range(8, 16)), (2, 3, 6, 7, 8, 10, 11, 13), (0, 1, 2, 3, 4, 5, 6, 15),
+            (1, 3, 5, 7, 9, 11, 13, 15), (0, 2, 4, 6, 8, 10, 12, 14)]
+PRECOMPILE_DECODE += [(0, 8, 14, 16, 8, 1, f, H, 1) for f, H in _IND_REP] + [(0, 8, 14, 16, 8, 0, 0, ids, 1) for ids in _IND_DEC]
 
 
 def _precompile_decode(args):
     import ctypes
     L = ctypes.CDLL(LIB)
     h = ctypes.c_void_p()
-    kind, k, d, n, w, op, lost, ids = args
+    kind, k, d, n, w, op, lost, ids = args[:8]
     rc = L.pmrc_create(ctypes.byref(h), kind, k, d, n, w)
+    if rc == 0 and len(args) > 8 and args[8]:
+        rc = L.pmrc_set_independent_launches(h, 1)
     if rc == 0:
         arr = (ctypes.c_int * len(ids))(*ids)
         n_ = ctypes.c_size_t(0)

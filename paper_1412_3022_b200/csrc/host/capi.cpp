@@ -225,6 +225,7 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "sync_groups") c->gen.sync_groups = v != 0;
         if (key == "cta_sync") c->gen.cta_sync = v;
         if (key == "dyn") c->gen.dyn = v;
+        if (key == "pdl") c->gen.pdl = v;
         if (key == "auto_wide16") c->gen.auto_wide16 = v != 0;
         if (key == "dyn_static") c->gen.dyn_static = v;
         if (key == "even_groups") c->gen.even_groups = v != 0;
@@ -835,6 +836,27 @@ int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *i
 int pmrc_set_max_ctas(pmrc_code *c, int max_ctas) {
   if (!c || max_ctas < 0) return fail(PMRC_EINVAL, "bad argument");
   c->max_ctas = max_ctas;
+  return PMRC_OK;
+}
+
+int pmrc_set_independent_launches(pmrc_code *c, int on) {
+  if (!c || on < 0 || on > 1) return fail(PMRC_EINVAL, "bad argument");
+  const int want = on ? 2 : 0;
+  if (c->gen.pdl == want) return PMRC_OK;
+  // the kernels are generated with or without griddepcontrol.wait: drop the built ones (they are
+  // rebuilt on next use, from the in-tree cubin cache when present) after the device is idle
+  if ((c->enc_built || !c->plans.empty()) && cudaDeviceSynchronize() != cudaSuccess) {
+    cudaGetLastError();
+    return fail(PMRC_ECUDA, "cudaDeviceSynchronize");
+  }
+  c->gen.pdl = want;
+  free_kernel(c->enc);
+  c->enc = Kernel();
+  c->enc_built = false;
+  for (auto &kv : c->plans) free_kernel(*kv.second);
+  c->plans.clear();
+  c->plan_meta.clear();
+  c->traced = nullptr;
   return PMRC_OK;
 }
 

@@ -924,6 +924,12 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
        "const u64 S, const u32 stripes, const u32 chunks, u64 *__restrict__ pace, const u32 epoch"
     << ((DYN || DYN0) ? ", u32 *__restrict__ dyn" : "") << ") {\n";
   s << "  extern __shared__ __align__(1024) unsigned char pm_smem[];\n";
+  if (o.pdl > 0) {
+    // programmatic dependent launch: let the next launch's CTAs be scheduled as this kernel's CTAs
+    // retire; pdl = 1 also waits for the preceding kernel's memory before touching global memory
+    s << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
+    if (o.pdl == 1) s << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+  }
   s << "  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, team = warp / PM_T, rank = warp - team * PM_T;\n";
   s << "  u32 dv_m, dv_s1, dv_s2;\n  pm_udiv_setup(chunks, dv_m, dv_s1, dv_s2);\n";
   int first_sid = -1;

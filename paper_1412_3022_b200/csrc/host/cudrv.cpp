@@ -19,6 +19,7 @@ const Drv &drv() {
     PM_SYM(CtxGetDevice, "cuCtxGetDevice");
     PM_SYM(DeviceGetAttribute, "cuDeviceGetAttribute");
     PM_SYM(LaunchKernel, "cuLaunchKernel");
+    PM_SYM(LaunchKernelEx, "cuLaunchKernelEx");
 #undef PM_SYM
     x.ok = x.GetErrorString && x.ModuleLoadData && x.ModuleUnload && x.ModuleGetFunction && x.FuncGetAttribute && x.FuncSetAttribute &&
            x.OccupancyMaxActiveBlocksPerMultiprocessor && x.CtxGetDevice && x.DeviceGetAttribute && x.LaunchKernel;

@@ -18,6 +18,7 @@ struct Drv {
   CUresult (*DeviceGetAttribute)(int *, CUdevice_attribute, CUdevice) = nullptr;
   CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            CUstream, void **, void **) = nullptr;
+  CUresult (*LaunchKernelEx)(const CUlaunchConfig *, CUfunction, void **, void **) = nullptr;  // optional (PDL)
 };
 const Drv &drv();
 }  // namespace pmrc

@@ -217,6 +217,7 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
   k.w = p.w == 16 ? 16 : 8;
   k.grid_ctas = oo.grid_ctas;
   k.teams = std::max(1, oo.warps / std::max(1, oo.team));
+  k.pdl = oo.pdl > 0;
   k.smem = (size_t)k.stats.smem_per_warp * oo.warps;
   std::vector<char> cubin;
   bool cached = false;
@@ -339,8 +340,23 @@ int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides
     const uint32_t epoch = ++k.epoch;
     void *dyn = k.dyn_on ? (void *)((uint32_t *)k.dyn + (size_t)(epoch % kDynSlots) * 2 * k.n_groups) : nullptr;
     void *args[] = {buf.data(), &S64, (void *)&ns, (void *)&chunks, &pace, (void *)&epoch, &dyn};
-    CUresult cr = drv().LaunchKernel((CUfunction)k.function, (unsigned)grid, 1, 1, k.tpb, 1, 1, (unsigned)k.smem, (CUstream)stream, args,
-                                 nullptr);
+    CUresult cr;
+    if (k.pdl && drv().LaunchKernelEx) {
+      CUlaunchAttribute at[1];
+      at[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+      at[0].value.programmaticStreamSerializationAllowed = 1;
+      CUlaunchConfig cfg = {};
+      cfg.gridDimX = (unsigned)grid; cfg.gridDimY = 1; cfg.gridDimZ = 1;
+      cfg.blockDimX = (unsigned)k.tpb; cfg.blockDimY = 1; cfg.blockDimZ = 1;
+      cfg.sharedMemBytes = (unsigned)k.smem;
+      cfg.hStream = (CUstream)stream;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cr = drv().LaunchKernelEx(&cfg, (CUfunction)k.function, args, nullptr);
+    } else {
+      cr = drv().LaunchKernel((CUfunction)k.function, (unsigned)grid, 1, 1, k.tpb, 1, 1, (unsigned)k.smem, (CUstream)stream,
+                              args, nullptr);
+    }
     if (cr != CUDA_SUCCESS) { err = "cuLaunchKernel: " + cu_err(cr); return PMRC_ECUDA; }
     launch_counter()++;
   }

@@ -50,6 +50,8 @@ struct GenOptions {
   int dyn = -1;             // layout 1: dynamic chunk schedule (per-group counters) instead of static
                             // ranges; 2: teams then help the other groups (-1 auto: 2 for clustered
                             // plans, i.e. decode, else 0)
+  int pdl = 0;               // programmatic dependent launch: 1 overlap launch only (wait for the
+                            // predecessor's memory first), 2 fully overlapped (independent launches)
   int dyn_static = 0;        // dyn >= 2: per mille of the chunks in static ranges (the rest: the counters)
   int cta_sync = 0;         // layout 1: all teams of a CTA start every item together (CTA barrier):
                             // the teams then fetch the same instructions at about the same time
@@ -122,7 +124,8 @@ struct Kernel {
   size_t pace_entries = 0;
   void *dyn = nullptr;              // layout 1 dynamic schedule: kDynSlots x n_groups x 2 u32 counters
   bool dyn_on = false;
-  bool dyn_full = false;            // stealing schedule: launched on the full grid (not G x spg)
+  bool dyn_full = false;
+  bool pdl = false;                 // launched with programmatic stream serialization            // stealing schedule: launched on the full grid (not G x spg)
   mutable uint32_t epoch = 0;       // launch epoch (counters carry it, so they never need a reset)
   size_t smem = 0;
   int blocks_per_sm = 1;

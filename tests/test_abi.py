@@ -139,6 +139,21 @@ def test_plan_stats_and_source_without_gpu():
         pm.pmrc_destroy(c)
 
 
+def test_independent_launches_flag_without_gpu():
+    c = pm.pmrc_create(pm.PMRC_MSR_SPARSE, 8, 14, 16)
+    try:
+        pm.pmrc_set_independent_launches(c, 1)     # nothing built yet: no device work
+        assert "griddepcontrol.launch_dependents" in pm.pmrc_encode_source(c)
+        assert "griddepcontrol.wait" not in pm.pmrc_encode_source(c)
+        pm.pmrc_set_independent_launches(c, 0)
+        assert "griddepcontrol" not in pm.pmrc_encode_source(c)
+        with pytest.raises(pm.PmrcError) as e:
+            pm.pmrc_set_independent_launches(c, 2)
+        assert e.value.rc == pm.PMRC_EINVAL
+    finally:
+        pm.pmrc_destroy(c)
+
+
 def test_prepare_plans_parallel_without_gpu():
     # config-4-style patterns compiled in parallel host threads (no GPU): singular helper sets (R10)
     # and all-systematic survivor sets are reported, the rest compile

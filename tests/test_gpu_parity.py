@@ -592,3 +592,43 @@ def test_decode_dynamic_schedule_concurrent_streams_and_tiny():
                 assert torch.equal(o, st.data), (S, stripes)
         finally:
             st.close()
+
+
+def test_independent_launches_per_stripe_repair_and_decode():
+    # config 4's per-stripe patterns with consecutive launches declared independent (programmatic
+    # dependent launch: a launch's CTAs start while the previous launch's CTAs retire)
+    k, n, S, stripes = 8, 16, 64 * 1024, 6
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=31)
+    try:
+        st.encode()
+        pm.pmrc_set_independent_launches(st.code, 1)
+        rep = [(0, 6, [0, 1, 2, 3, 4, 5, 7, 8, 9, 10, 11, 13, 14, 15]),
+               (1, 15, [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 11, 12, 13, 14]),
+               (2, 8, [0, 1, 2, 3, 4, 5, 6, 9, 10, 11, 12, 13, 14, 15]),
+               (3, 3, [0, 1, 2, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14]),
+               (4, 12, [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 13, 14]),
+               (5, 0, [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 15])]
+        dec = [(t, ids) for t, ids in enumerate(([0, 1, 4, 5, 9, 12, 14, 15], list(range(8, 16)),
+                                                 [2, 3, 6, 7, 8, 10, 11, 13], [0, 1, 2, 3, 4, 5, 6, 15],
+                                                 [1, 3, 5, 7, 9, 11, 13, 15], [0, 2, 4, 6, 8, 10, 12, 14]))]
+        a = st.alpha
+        out = torch.full((stripes, a, S), 0xAB, dtype=torch.uint8, device=DEV)
+        dout = st.data.clone()
+        for t, ids in dec:
+            for i in range(k):
+                if i not in ids:
+                    dout[t, i * a:(i + 1) * a] = 0xCC
+        for rnd in range(3):
+            for t, f, H in rep:
+                pcs = [(p + t * s_, s_) for p, s_ in (st.piece(i) for i in H)]
+                pm.pmrc_repair(st.code, f, H, pcs, (out[t].data_ptr(), a * S), S, 1, st.stream)
+            for t, ids in dec:
+                pcs = [(p + t * s_, s_) for p, s_ in (st.piece(i) for i in ids)]
+                pm.pmrc_decode(st.code, ids, pcs, dout[t].data_ptr(), S, 1, st.stream)
+        torch.cuda.synchronize()
+        for t, f, _ in rep:
+            assert torch.equal(out[t], st.piece_tensor(f)[t]), (t, f)
+        assert torch.equal(dout, st.data)
+        pm.pmrc_set_independent_launches(st.code, 0)
+    finally:
+        st.close()

@@ -115,7 +115,10 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     // 767 -> 822 GB/s); with <= 3 idle SMs static ranges measured better (GF(2^8) k=8: 7 groups)
     GenStats g2;
     (void)generate_source(p, oo, g2);
-    oo.dyn = (oo.layout == 1 && g2.groups > 1 && 148 % g2.groups >= 4) ? 2 : 0;
+    // ... and single-group plans of >= 3 stages (parity-node repair, 98 blocks in 7 stages: 0.405 ->
+    // 0.387 ms; one-stage single-group plans, RS encode and systematic-node repair, measured slower)
+    oo.dyn = (oo.layout == 1 && ((g2.groups > 1 && 148 % g2.groups >= 4) || (g2.groups == 1 && g2.max_stages >= 3)))
+                 ? 2 : 0;
   }
   if (oo.ws) {  // ws_prod producers + 2 consumers per team, <= 4 teams (4 named barriers each), 2 buffers
     oo.team = std::max(1, oo.ws_prod) + 2;

@@ -225,6 +225,7 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
         if (key == "sync_groups") c->gen.sync_groups = v != 0;
         if (key == "cta_sync") c->gen.cta_sync = v;
         if (key == "dyn") c->gen.dyn = v;
+        if (key == "smem_kib") c->gen.smem_kib = v;
         if (key == "pdl") c->gen.pdl = v;
         if (key == "auto_wide16") c->gen.auto_wide16 = v != 0;
         if (key == "dyn_static") c->gen.dyn_static = v;

@@ -128,12 +128,16 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
   // warps per CTA from the shared-memory budget (2 stage buffers of in_block KiB per team)
   GenStats probe;
   (void)generate_source(p, oo, probe);
-  int budget = 220 * 1024;
+  // 225 KiB of stage buffers (+ 1 KiB alignment reservation + the schedule slots <= 227 KiB): 16 warps
+  // (8 teams of 2) with the k=8 encode's 14-block stages (224 KiB)
+  int budget = o.smem_kib > 0 ? o.smem_kib * 1024 : 225 * 1024;
   int w = std::max(1, std::min(32, budget / std::max(1, probe.smem_per_warp)));
-  // 12 warps (6 teams of 2): measured best for encode, and for the multi-stage repair plans
-  // (config-4 repair 0.421 -> 0.404 ms vs 8 warps); wide decode plans set 16 above (auto_wide)
+  // 16 warps when they fit: measured against 12 (the previous default, whose 220 KiB budget left the
+  // encode at 12): MSR k=8 encode 0.528 -> 0.501 ms, MBR k=8 0.597 -> 0.568, parity-node repair
+  // 0.387 -> 0.358, GF(2^16) k=8 1.359 -> 1.218, RS 0.345 -> 0.340; MSR k=4 and vanilla unchanged;
+  // 14 warps measured worse (0.571)
   int want = oo.warps;
-  if (want <= 0) want = 12;
+  if (want <= 0) want = 16;
   w = std::min(w, want);
   w = std::max(oo.team, w - w % std::max(1, oo.team));  // whole teams
   oo.warps = w;

@@ -52,6 +52,7 @@ struct GenOptions {
                             // plans, i.e. decode, else 0)
   int pdl = 0;               // programmatic dependent launch: 1 overlap launch only (wait for the
                             // predecessor's memory first), 2 fully overlapped (independent launches)
+  int smem_kib = 0;          // shared-memory budget per CTA for the warp count (0 = 220 KiB)
   int dyn_static = 0;        // dyn >= 2: per mille of the chunks in static ranges (the rest: the counters)
   int cta_sync = 0;         // layout 1: all teams of a CTA start every item together (CTA barrier):
                             // the teams then fetch the same instructions at about the same time

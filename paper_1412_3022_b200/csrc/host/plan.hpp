@@ -74,6 +74,7 @@ struct GenOptions {
   bool auto_wide16 = true;   // resolve_options: 16-row groups on 4-warp teams, layout 0, for many
                              // groups whose supports have >= 16 rows (k = 16 encode)
   bool auto_wide = true;    // resolve_options: 16-row groups on 4-warp teams for wide multi-stage plans
+  int enc_restarts = 4;     // CSE restarts for the encode plan (built once per code; capi.cpp)
   int cse_restarts = 1;     // CSE runs per network (seeded near-tie randomisation), keep the cheapest
   bool sched = false;       // register-pressure-aware temp order (emit_slp_sched) instead of CSE order
   int l2_shared = 0;        // layouts 1/2: L2 policy of blocks read by >1 group (-1 static last-read rule, 0 normal, 2 evict_last)

@@ -89,20 +89,55 @@ class ClockSampler:
                 "reasons": sorted(self.reasons)}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def cpu_baseline(stripes_sample=4):
-    """The oracle as it stands, single thread, on the first `stripes_sample` stripes of the same
-    workload (same bytes: the shared generator)."""
-    import numpy as np
+    """The oracle as it stands (plain C, scalar log/exp tables, never tuned) on the same workload's
+    bytes (the shared seeded generator), on the box's host cores:
+      * all cores: one host thread per core over the 19 stripes of the full 1 GiB job (ctypes
+        releases the GIL inside the C call, so the threads run in parallel);
+      * one core: the first `stripes_sample` stripes, the paper's own setting (one core)."""
+    import concurrent.futures as cf
     import inputs
     import oracle as O
     B = 56
-    x = inputs.stripe_data(stripes_sample, B, S_, seed=1234, real_len=REAL)
+    stripes = -(-REAL // (B * S_))
+    cores = os.cpu_count() or 1
+    x1 = inputs.stripe_data(stripes_sample, B, S_, seed=1234, real_len=REAL)
     t0 = time.perf_counter()
-    O.encode(O.MSR_SPARSE, N_, K_, D_, x)
-    dt = time.perf_counter() - t0
-    return {"value": x.size / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": "%d of 19 stripes (%d MiB of source), plain C scalar log/exp oracle, 1 thread" %
-                      (stripes_sample, x.size >> 20), "seconds": round(dt, 2)}
+    O.encode(O.MSR_SPARSE, N_, K_, D_, x1)
+    dt1 = time.perf_counter() - t0
+    del x1
+
+    def one(t):
+        x = inputs.stripe_data(1, B, S_, seed=1234, t0=t, real_len=REAL)
+        t_ = time.perf_counter()
+        O.encode(O.MSR_SPARSE, N_, K_, D_, x)
+        return time.perf_counter() - t_
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=cores) as ex:
+        list(ex.map(one, range(stripes)))
+    dtn = time.perf_counter() - t0     # wall time of the parallel pass (includes host data generation)
+    return {"value": REAL / dtn / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "sample": "all %d stripes of the 1 GiB job (1064 MiB processed, R11), one host thread per core, "
+                      "plain C scalar log/exp oracle" % stripes,
+            "seconds": round(dtn, 2), "cpu_model": cpu_model(), "os_cpu_count": os.cpu_count(),
+            "single_core": {"value": x_bytes(stripes_sample, B) / dt1 / 1e9, "unit": "GB/s", "cores": 1,
+                            "sample": "%d of %d stripes (%d MiB of source), 1 thread (the paper's setting, P:214)" %
+                                      (stripes_sample, stripes, x_bytes(stripes_sample, B) >> 20),
+                            "seconds": round(dt1, 2)}}
+
+
+def x_bytes(stripes, B):
+    return stripes * B * S_
 
 
 def run_reference(args):
@@ -134,6 +169,38 @@ def run_reference(args):
     return 0
 
 
+def spawn_ranks(args):
+    """`python bench.py --gpus N` outside torchrun: re-launch this script as N ranks (one process
+    per GPU) through torch.distributed.run on 127.0.0.1, exactly as the driver does, and return its
+    exit code.  Inside torchrun (WORLD_SIZE set) the world size must equal --gpus."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def launch_check(args):
+    """--launch-check: the multi-rank plumbing alone (gloo, CPU): every rank joins, rank 0 prints
+    the world it saw.  Used by tests/test_bench_launcher.py to drive the launcher end to end."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([1.0])
+    if world > 1:
+        dist.all_reduce(t)
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "ranks_joined": int(t.item()),
+                          "gpus_flag": args.gpus}))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -142,9 +209,19 @@ def main():
     ap.add_argument("--impl", default="pmrc", choices=["pmrc", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args)
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env != args.gpus:
+        sys.stderr.write("bench.py: --gpus %d but WORLD_SIZE=%d: refusing to report a mismatched n_gpus\n"
+                         % (args.gpus, world_env))
+        return 2
+    if args.launch_check:
+        return launch_check(args)
 
     import torch
     import torch.distributed as dist
@@ -257,8 +334,8 @@ def main():
         del hd, hp
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline()
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline()     # rank 0 only, after every rank's timed region
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,

@@ -56,7 +56,9 @@ enum {
 enum {
   PMRC_OK = 0,
   PMRC_EINVAL = -1,       /* null pointer, id out of range / duplicated, wrong counts */
-  PMRC_EUNSUPPORTED = -2, /* w != 8; MSR with d != 2k-2; field too small; invalid construction */
+  PMRC_EUNSUPPORTED = -2, /* w not in {8, 16} (w = 16: sparse MSR only, and not for pmrc_apply /
+                             the split repair calls); MSR with d != 2k-2; field too small;
+                             invalid construction */
   PMRC_ESINGULAR = -3,    /* survivors do not span the data / helper matrix Psi_H singular (R10) */
   PMRC_EALIGN = -4,       /* S % 16 != 0 or a block address not 16-byte aligned */
   PMRC_ENOMEM = -5,       /* host or device allocation failed */
@@ -159,12 +161,20 @@ int pmrc_set_max_ctas(pmrc_code *c, int max_ctas);
 
 /* on = 1: the caller guarantees that consecutive launches of this handle on a stream are
  * independent (none reads or writes what the preceding one writes, e.g. config 4's per-stripe
- * repairs / decodes of different stripes).  Kernels are then launched with programmatic dependent
- * launch (cuLaunchKernelEx, PROGRAMMATIC_STREAM_SERIALIZATION) and let the next launch's CTAs start
- * as this launch's CTAs retire, so a small launch does not pay a full-GPU ramp and tail (measured
- * config-4 per-stripe repair 0.517 -> 0.348 ms).  A launch that follows a kernel of another library
- * still waits for it to complete.  on = 0 (default): ordinary stream order.  Synchronises the device
- * and drops the handle's built kernels (rebuilt on next use).  PMRC_EINVAL for other values. */
+ * repairs / decodes of different stripes when issued one launch per stripe).  Kernels are then
+ * launched with programmatic dependent launch (cuLaunchKernelEx, PROGRAMMATIC_STREAM_SERIALIZATION)
+ * and trigger their dependents on entry without waiting for their predecessor, so the next
+ * launch's CTAs start as this launch's CTAs retire and a small launch does not pay a full-GPU
+ * ramp and tail (measured config-4 per-stripe repair 0.517 -> 0.348 ms).
+ * Ordering contract: the launch is ordered after a preceding kernel of another library only if
+ * that kernel does NOT itself trigger programmatic completion early (griddepcontrol.launch_dependents
+ * / cudaTriggerProgrammaticLaunchCompletion before its last store); kernels without such a trigger
+ * (the default for every non-PDL kernel) complete before the launch starts.  When the preceding
+ * work may trigger early (another handle with independent launches on, a PDL-enabled library
+ * kernel), separate the two with an event wait or a non-PDL launch.  The batch calls
+ * (pmrc_decode_batch / pmrc_repair_batch) run per-stripe patterns in ONE launch and need none of
+ * this.  on = 0 (default): ordinary stream order.  Synchronises the device and drops the handle's
+ * built kernels (rebuilt on next use).  PMRC_EINVAL for other values. */
 int pmrc_set_independent_launches(pmrc_code *c, int on);
 
 /* Blocks each helper reads to repair lost_id: nnz(phi_f) (MSR: 1 if f < alpha else alpha,

@@ -1,7 +1,8 @@
 """CPU oracle for the product-matrix regenerating-code hot path (arxiv 1412.3022).
 
-TEST INFRASTRUCTURE ONLY: only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
-``cpu_baseline`` / ``--impl reference`` legs may import this package.  The product path
+TEST INFRASTRUCTURE ONLY: only ``tests/``, ``__graft_entry__.smoke()``, ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs and the measurement tools' sampled correctness
+checks (``tools/sweep.py``) may import this package.  The product path
 (``paper_1412_3022_b200``) shares no code with it and never calls it.
 
 Thin ctypes/numpy wrapper over ``pmrc_oracle.c`` (plain scalar log/exp GF(2^8) arithmetic,
@@ -63,6 +64,7 @@ def _lib():
             "or_repair_reads": ([I, I, I, I, I], I),
             "or_repair_project": ([I, I, I, I, I, P, P, Z], I),
             "or_validate16_sparse": ([I, ctypes.POINTER(ctypes.c_int)], I),
+            "or_validate16_sparse_n": ([I, I, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)], I),
             "or_gf16_mul": ([ctypes.c_uint16, ctypes.c_uint16], ctypes.c_uint16),
             "or_repair_combine": ([I, I, I, I, I, P, P, P, Z], I),
             "or_repair": ([I, I, I, I, I, P, P, P, Z], I),
@@ -285,6 +287,14 @@ def validate16_sparse(k):
     f = ctypes.c_int(0)
     _chk(_lib().or_validate16_sparse(k, ctypes.byref(f)), "validate16_sparse")
     return f.value
+
+
+def validate16_sparse_n(k, n):
+    """The same check over EVERY d-row subset at n = d+1 or n = d+2 (= 2k): (flags, number of
+    singular d-subsets)."""
+    f, ns = ctypes.c_int(0), ctypes.c_int(0)
+    _chk(_lib().or_validate16_sparse_n(k, n, ctypes.byref(f), ctypes.byref(ns)), "validate16_sparse_n")
+    return f.value, ns.value
 
 
 def repair_combine(kind, n, k, d, f, H, betas):

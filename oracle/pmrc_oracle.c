@@ -2,8 +2,8 @@
  * pmrc_oracle.c — plain, slow, obviously-correct CPU oracle for the product-matrix
  * regenerating-code hot path of arxiv 1412.3022 ("Fast Product-Matrix Regenerating Codes").
  *
- * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
- * --impl reference legs may load this library.  The product (paper_1412_3022_b200/, include/)
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke(), bench.py's cpu_baseline /
+ * --impl reference legs and the sampled correctness checks of tools/sweep.py may load this library.  The product (paper_1412_3022_b200/, include/)
  * shares no code with it and never calls it.
  *
  * Citations:  P:L = /root/reference/PAPER.md line L (section), S:L = SPEC.md line L.
@@ -902,10 +902,18 @@ static int gf16_rank(uint16_t *W, int r, int c) {
 }
 uint16_t or_gf16_mul(uint16_t a, uint16_t b) { gf16_init(); return gf16_mul(a, b); }
 
-int or_validate16_sparse(int k, int *flags_out) {
+/* P:189 validity check of the sparse MSR code over GF(2^16) at n = d+1 (the n d-subsets the paper
+ * checks) -- or, through or_validate16_sparse_n, at n = d+1 or d+2 over EVERY d-row subset (all
+ * rows but one / but two), counting the singular ones (SURVEY §8(c) A7 predicts exactly the
+ * C(alpha, 2) subsets that omit two identity rows at n = 2k, k >= 3). */
+int or_validate16_sparse_n(int k, int n, int *flags_out, int *n_singular);
+int or_validate16_sparse(int k, int *flags_out) { return or_validate16_sparse_n(k, 2 * k - 1, flags_out, 0); }
+
+int or_validate16_sparse_n(int k, int n, int *flags_out, int *n_singular) {
   gf16_init();
   if (k < 2 || k > 200) return OR_EINVAL;
-  const int alpha = k - 1, d = 2 * k - 2, n = d + 1;
+  const int alpha = k - 1, d = 2 * k - 2;
+  if (n < d + 1 || n > d + 2) return OR_EINVAL;
   uint16_t *psi = (uint16_t *)malloc(sizeof(uint16_t) * n * d), *lam = (uint16_t *)malloc(sizeof(uint16_t) * n);
   uint16_t *M = (uint16_t *)malloc(sizeof(uint16_t) * d * d);
   for (int i = 1; i <= n; i++) {
@@ -922,13 +930,20 @@ int or_validate16_sparse(int k, int *flags_out) {
   for (int a = 0; a < n; a++)
     for (int b = 0; b < a; b++)
       if (lam[a] == lam[b]) flags |= 1;
-  for (int skip = 0; skip < n && !(flags & 2); skip++) { /* the n d-subsets: all rows but one */
-    int r = 0;
-    for (int i = 0; i < n; i++)
-      if (i != skip) memcpy(M + (size_t)(r++) * d, psi + (size_t)i * d, sizeof(uint16_t) * d);
-    if (gf16_rank(M, d, d) < d) flags |= 2;
-  }
+  int sing = 0;
+  for (int s1 = 0; s1 < n; s1++) /* every d-subset: all rows but {s1} (n = d+1) or {s1, s2} (n = d+2) */
+    for (int s2 = (n == d + 2 ? s1 + 1 : n); s2 <= n; s2++) {
+      if (n == d + 2 && s2 == n) continue;
+      int r = 0;
+      for (int i = 0; i < n; i++)
+        if (i != s1 && i != s2) memcpy(M + (size_t)(r++) * d, psi + (size_t)i * d, sizeof(uint16_t) * d);
+      if (gf16_rank(M, d, d) < d) {
+        flags |= 2;
+        sing++;
+      }
+    }
   free(psi); free(lam); free(M);
   *flags_out = flags;
+  if (n_singular) *n_singular = sing;
   return OR_OK;
 }

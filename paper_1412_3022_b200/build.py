@@ -1,8 +1,10 @@
-"""In-tree build of libpmrc.so (host C++ + NVRTC JIT) and the shared input generator.
+"""In-tree build of libpmrc.so (host C++ + NVRTC JIT of the generated bitsliced kernels, and the
+nvcc-compiled runtime-coefficient kernels of csrc/rt/) and the shared input generator.
 
 The bitsliced kernels are generated per plan and compiled by NVRTC for sm_100a at
-``pmrc_create`` / first use (``-arch=sm_100a``); ``build()`` also nvcc-compiles the generated
-encode kernels of the benchmark configurations for sm_100a as a compile check and SASS artefact.
+``pmrc_create`` / first use (``-arch=sm_100a``); ``build()`` pre-compiles the encode kernels of the
+benchmark configurations and the decode / repair plans the GPU tests use into the in-tree kernel
+cache (``kcache/``), so the GPU box loads cubins instead of running NVRTC.
 """
 import os
 import subprocess

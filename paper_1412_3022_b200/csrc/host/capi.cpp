@@ -27,12 +27,12 @@ int fail(int rc, const std::string &msg) {
 
 constexpr int kHostBufs = 3;  // staging ring: H2D of chunk i+1/i+2 overlaps compute and D2H of chunk i
 struct HostStage {
-  size_t chunk_stripes = 0;
+  size_t data_bytes = 0;  // allocated size of each d_data[i] (bytes, not stripes: S may change
+  size_t par_bytes = 0;   //   between calls on one handle) / of each d_par[i]
   void *d_data[kHostBufs] = {};
   void *d_par[kHostBufs] = {};
   cudaStream_t st[kHostBufs] = {};
   cudaEvent_t ev_start = nullptr;
-  size_t bytes = 0;
 };
 }  // namespace
 
@@ -185,6 +185,100 @@ bool repair_matrix(const CodeDef &d, int f, const int *H, Mat &R) {
   return true;
 }
 
+// (id, region) pairs sorted by id: plans and their cache keys depend on id sets, not orders
+void canonical_order(const int *ids, const pmrc_cregion *regs, int n, std::vector<int> &ids_out,
+                     std::vector<pmrc_cregion> &regs_out) {
+  std::vector<int> perm(n);
+  for (int i = 0; i < n; i++) perm[i] = i;
+  std::sort(perm.begin(), perm.end(), [&](int a, int b) { return ids[a] < ids[b]; });
+  ids_out.resize(n);
+  regs_out.resize(n);
+  for (int i = 0; i < n; i++) {
+    ids_out[i] = ids[perm[i]];
+    regs_out[i] = regs[perm[i]];
+  }
+}
+
+// PMRC_GEN parser (see pmrc_create).  Only result-preserving generator options are accepted.
+int apply_gen_knobs(const std::string &s, GenOptions &G, std::string &err) {
+  struct Knob {
+    const char *key;
+    int min;
+    void (*set)(GenOptions &, int);
+  };
+  static const Knob knobs[] = {
+      {"max_rows", 1, [](GenOptions &o, int v) { o.max_rows = v; }},
+      {"in_block", 1, [](GenOptions &o, int v) { o.in_block = v; }},
+      {"warps", 1, [](GenOptions &o, int v) { o.warps = v; }},
+      {"cse", 0, [](GenOptions &o, int v) { o.cse = v != 0; }},
+      {"sync_groups", 0, [](GenOptions &o, int v) { o.sync_groups = v != 0; }},
+      {"cta_sync", 0, [](GenOptions &o, int v) { o.cta_sync = v; }},
+      {"dyn", -1, [](GenOptions &o, int v) { o.dyn = v; }},
+      {"enc_restarts", 1, [](GenOptions &o, int v) { o.enc_restarts = v; }},
+      {"smem_kib", 0, [](GenOptions &o, int v) { o.smem_kib = v; }},
+      {"pdl", 0, [](GenOptions &o, int v) { o.pdl = v; }},
+      {"auto_wide16", 0, [](GenOptions &o, int v) { o.auto_wide16 = v != 0; }},
+      {"dyn_static", 0, [](GenOptions &o, int v) { o.dyn_static = v; }},
+      {"even_groups", 0, [](GenOptions &o, int v) { o.even_groups = v != 0; }},
+      {"tr_balance", 0, [](GenOptions &o, int v) { o.tr_balance = v != 0; }},
+      {"cluster_wide", 0, [](GenOptions &o, int v) { o.cluster_wide = v != 0; }},
+      {"balance_ranks", 0, [](GenOptions &o, int v) { o.balance_ranks = v != 0; }},
+      {"ld_hint", 0, [](GenOptions &o, int v) { o.ld_hint = v; }},
+      {"chunk_loop", 1, [](GenOptions &o, int v) { o.chunk_loop = v; }},
+      {"team", 1, [](GenOptions &o, int v) { o.team = v; }},
+      {"fold", 0, [](GenOptions &o, int v) { o.fold = v != 0; }},
+      {"layout", -1, [](GenOptions &o, int v) { o.layout = v; }},
+      {"pace_lag", 0, [](GenOptions &o, int v) { o.pace_lag = v; }},
+      {"trace", 0, [](GenOptions &o, int v) { o.trace = v != 0; }},
+      {"net_in", 0, [](GenOptions &o, int v) { o.net_in = v; }},
+      {"net_even", 0, [](GenOptions &o, int v) { o.net_even = v != 0; }},
+      {"stage_even", 0, [](GenOptions &o, int v) { o.stage_even = v != 0; }},
+      {"fence", 0, [](GenOptions &o, int v) { o.fence = v != 0; }},
+      {"tr_unroll", 1, [](GenOptions &o, int v) { o.tr_unroll = v; }},
+      {"sched", 0, [](GenOptions &o, int v) { o.sched = v != 0; }},
+      {"cse_restarts", 1, [](GenOptions &o, int v) { o.cse_restarts = v; }},
+      {"auto_wide", 0, [](GenOptions &o, int v) { o.auto_wide = v != 0; }},
+      {"nbuf", 2, [](GenOptions &o, int v) { o.nbuf = v; }},
+      {"own_first", 0, [](GenOptions &o, int v) { o.own_first = v != 0; }},
+      {"l2_shared", -1, [](GenOptions &o, int v) { o.l2_shared = v; }},
+      {"ws", 0, [](GenOptions &o, int v) { o.ws = v != 0; }},
+      {"ws_prod", 1, [](GenOptions &o, int v) { o.ws_prod = v; }},
+      {"grid_ctas", 1, [](GenOptions &o, int v) { o.grid_ctas = v; }},
+  };
+  std::string applied;
+  size_t pos = 0;
+  while (pos < s.size()) {
+    size_t e = s.find(',', pos);
+    if (e == std::string::npos) e = s.size();
+    const std::string kv = s.substr(pos, e - pos);
+    pos = e + 1;
+    if (kv.empty()) continue;
+    const size_t eq = kv.find('=');
+    char *end = nullptr;
+    const long v = eq == std::string::npos ? 0 : strtol(kv.c_str() + eq + 1, &end, 10);
+    if (eq == std::string::npos || end == kv.c_str() + eq + 1 || *end) {
+      err = "PMRC_GEN: malformed entry '" + kv + "' (want key=integer)";
+      return PMRC_EINVAL;
+    }
+    const std::string key = kv.substr(0, eq);
+    const Knob *k = nullptr;
+    for (const Knob &kn : knobs)
+      if (key == kn.key) k = &kn;
+    if (!k) {
+      err = "PMRC_GEN: unknown generator knob '" + key + "'";
+      return PMRC_EINVAL;
+    }
+    if (v < k->min || v > (1 << 20)) {
+      err = "PMRC_GEN: value out of range in '" + kv + "'";
+      return PMRC_EINVAL;
+    }
+    k->set(G, (int)v);
+    applied += (applied.empty() ? "" : ",") + kv;
+  }
+  err = "PMRC_GEN applied: " + applied;
+  return PMRC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -214,59 +308,15 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
   if (!c) return fail(PMRC_ENOMEM, "host allocation");
   std::string err;
   if (kind == KIND_RS) d = k;
-  // tuning knob (experiments only): PMRC_GEN="max_rows=8,in_block=16,tpb=256,cse=1"
+  // generator tuning knobs (experiments only): PMRC_GEN="max_rows=8,in_block=16,warps=16".  Every
+  // knob selects among code-generation strategies that compute the same result (the bitsliced
+  // networks are exact whatever the grouping, staging, schedule or warp count); an unknown key or
+  // a malformed entry fails pmrc_create with PMRC_EINVAL, so a typo or a stale knob cannot pass
+  // silently.  The applied knobs are readable through pmrc_last_error() right after pmrc_create.
   if (const char *g = getenv("PMRC_GEN")) {
-    std::string s = g;
-    size_t pos = 0;
-    while (pos < s.size()) {
-      size_t e = s.find(',', pos);
-      if (e == std::string::npos) e = s.size();
-      std::string kv = s.substr(pos, e - pos);
-      size_t eq = kv.find('=');
-      if (eq != std::string::npos) {
-        std::string key = kv.substr(0, eq);
-        int v = atoi(kv.c_str() + eq + 1);
-        if (key == "max_rows" && v > 0) c->gen.max_rows = v;
-        if (key == "in_block" && v > 0) c->gen.in_block = v;
-        if (key == "warps" && v >= 1) c->gen.warps = v;
-        if (key == "cse") c->gen.cse = v != 0;
-        if (key == "sync_groups") c->gen.sync_groups = v != 0;
-        if (key == "cta_sync") c->gen.cta_sync = v;
-        if (key == "dyn") c->gen.dyn = v;
-        if (key == "enc_restarts") c->gen.enc_restarts = v;
-        if (key == "smem_kib") c->gen.smem_kib = v;
-        if (key == "pdl") c->gen.pdl = v;
-        if (key == "auto_wide16") c->gen.auto_wide16 = v != 0;
-        if (key == "dyn_static") c->gen.dyn_static = v;
-        if (key == "even_groups") c->gen.even_groups = v != 0;
-        if (key == "tr_balance") c->gen.tr_balance = v != 0;
-        if (key == "cluster_wide") c->gen.cluster_wide = v != 0;
-        if (key == "balance_ranks") c->gen.balance_ranks = v != 0;
-        if (key == "ld_hint") c->gen.ld_hint = v;
-        if (key == "chunk_loop" && v > 0) c->gen.chunk_loop = v;
-        if (key == "team" && v > 0) c->gen.team = v;
-        if (key == "fold") c->gen.fold = v != 0;
-        if (key == "layout") c->gen.layout = v;
-        if (key == "pace_lag") c->gen.pace_lag = v;
-        if (key == "trace") c->gen.trace = v != 0;
-        if (key == "net_in") c->gen.net_in = v;
-        if (key == "net_even") c->gen.net_even = v != 0;
-        if (key == "stage_even") c->gen.stage_even = v != 0;
-        if (key == "fence") c->gen.fence = v != 0;
-        if (key == "tr_unroll" && v > 0) c->gen.tr_unroll = v;
-        if (key == "sched") c->gen.sched = v != 0;
-        if (key == "cse_restarts" && v > 0) c->gen.cse_restarts = v;
-        if (key == "auto_wide") c->gen.auto_wide = v != 0;
-        if (key == "nbuf" && v >= 2) c->gen.nbuf = v;
-        if (key == "own_first") c->gen.own_first = v != 0;
-        if (key == "debug") c->gen.debug = v;
-        if (key == "l2_shared") c->gen.l2_shared = v;
-        if (key == "ws") c->gen.ws = v != 0;
-        if (key == "ws_prod" && v > 0) c->gen.ws_prod = v;
-        if (key == "grid_ctas" && v > 0) c->gen.grid_ctas = v;
-      }
-      pos = e + 1;
-    }
+    int rc0 = apply_gen_knobs(g, c->gen, err);
+    if (rc0) return fail(rc0, err);
+    g_last_error = err;
   }
   int rc;
   if (w == 16) {
@@ -519,18 +569,29 @@ int pmrc_encode_host(pmrc_code *c, const void *data_host, void *parity_host, siz
   // chunks of ~64 MiB of source data, a ring of kHostBufs buffers / streams
   size_t chunk = std::max<size_t>(1, ((size_t)64 << 20) / in_b);
   chunk = std::min(chunk, stripes);
-  if (h.chunk_stripes < chunk) {
+  if (h.data_bytes < chunk * in_b || h.par_bytes < chunk * out_b) {
+    // (re)allocate by byte size: a later call with a larger S must not reuse smaller buffers
     for (int i = 0; i < kHostBufs; i++) {
+      if (h.d_data[i] && cudaStreamSynchronize(h.st[i]) != cudaSuccess) cudaGetLastError();
       if (h.d_data[i]) cudaFree(h.d_data[i]);
       if (h.d_par[i]) cudaFree(h.d_par[i]);
       h.d_data[i] = h.d_par[i] = nullptr;
-      if (cudaMalloc(&h.d_data[i], chunk * in_b) != cudaSuccess || cudaMalloc(&h.d_par[i], chunk * out_b) != cudaSuccess) {
+    }
+    h.data_bytes = h.par_bytes = 0;
+    const size_t nd = std::max(h.data_bytes, chunk * in_b), np = std::max(h.par_bytes, chunk * out_b);
+    for (int i = 0; i < kHostBufs; i++) {
+      if (cudaMalloc(&h.d_data[i], nd) != cudaSuccess || cudaMalloc(&h.d_par[i], np) != cudaSuccess) {
         cudaGetLastError();
-        h.chunk_stripes = 0;
+        for (int j = 0; j <= i; j++) {
+          if (h.d_data[j]) cudaFree(h.d_data[j]);
+          if (h.d_par[j]) cudaFree(h.d_par[j]);
+          h.d_data[j] = h.d_par[j] = nullptr;
+        }
         return fail(PMRC_ENOMEM, "staging buffers");
       }
     }
-    h.chunk_stripes = chunk;
+    h.data_bytes = nd;
+    h.par_bytes = np;
   }
   for (int i = 0; i < kHostBufs; i++)
     if (!h.st[i] && cudaStreamCreateWithFlags(&h.st[i], cudaStreamNonBlocking) != cudaSuccess)
@@ -673,12 +734,19 @@ static int decode_spec16(const pmrc_code *c, const int *surv_ids, int n_surv, Pl
   return PMRC_OK;
 }
 
-int pmrc_decode(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregion *pieces, void *data_out, size_t S,
-                size_t stripes, int *n_written, void *stream) {
+int pmrc_decode(pmrc_code *c, const int *surv_ids_in, int n_surv, const pmrc_cregion *pieces_in, void *data_out,
+                size_t S, size_t stripes, int *n_written, void *stream) {
   if (n_written) *n_written = 0;
-  if (!c || !surv_ids || !pieces || !data_out) return fail(PMRC_EINVAL, "NULL argument");
+  if (!c || !surv_ids_in || !pieces_in || !data_out) return fail(PMRC_EINVAL, "NULL argument");
   const CodeDef &D = c->def;
-  if (n_surv < 1 || n_surv > D.n || check_ids(D, surv_ids, n_surv)) return fail(PMRC_EINVAL, "bad survivor ids");
+  if (n_surv < 1 || n_surv > D.n || check_ids(D, surv_ids_in, n_surv)) return fail(PMRC_EINVAL, "bad survivor ids");
+  // canonical order: the plan (and its cache key) depends on the survivor SET only; the pieces are
+  // permuted with the ids (the decoded data is unique, so the order cannot change it)
+  std::vector<int> surv_v;
+  std::vector<pmrc_cregion> pieces_v;
+  canonical_order(surv_ids_in, pieces_in, n_surv, surv_v, pieces_v);
+  const int *surv_ids = surv_v.data();
+  const pmrc_cregion *pieces = pieces_v.data();
   if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
   const std::string key = ids_key("dec", surv_ids, n_surv, 0);
   auto fe = c->plan_err.find(key);
@@ -891,12 +959,18 @@ static int repair_common(pmrc_code *c, int lost_id, const int *helper_ids, int n
   return PMRC_OK;
 }
 
-int pmrc_repair(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers, const pmrc_cregion *helper_pieces,
-                pmrc_region out_piece, size_t S, size_t stripes, void *stream) {
-  if (!c || !helper_ids || !helper_pieces) return fail(PMRC_EINVAL, "NULL argument");
+int pmrc_repair(pmrc_code *c, int lost_id, const int *helper_ids_in, int n_helpers,
+                const pmrc_cregion *helper_pieces_in, pmrc_region out_piece, size_t S, size_t stripes, void *stream) {
+  if (!c || !helper_ids_in || !helper_pieces_in) return fail(PMRC_EINVAL, "NULL argument");
   int need = 0;
-  int rc = repair_common(c, lost_id, helper_ids, n_helpers, &need);
+  int rc = repair_common(c, lost_id, helper_ids_in, n_helpers, &need);
   if (rc) return rc;
+  // canonical helper order (the plan depends on the helper SET; the repaired piece is unique)
+  std::vector<int> help_v;
+  std::vector<pmrc_cregion> hp_v;
+  canonical_order(helper_ids_in, helper_pieces_in, n_helpers, help_v, hp_v);
+  const int *helper_ids = help_v.data();
+  const pmrc_cregion *helper_pieces = hp_v.data();
   if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
   const CodeDef &D = c->def;
   const std::string key = ids_key("rep", helper_ids, n_helpers, lost_id);
@@ -1044,13 +1118,18 @@ int pmrc_repair_project(pmrc_code *c, int lost_id, pmrc_cregion piece, pmrc_regi
   return PMRC_OK;
 }
 
-int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids, int n_helpers, const pmrc_cregion *betas,
-                        pmrc_region out_piece, size_t S, size_t stripes, void *stream) {
+int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids_in, int n_helpers,
+                        const pmrc_cregion *betas_in, pmrc_region out_piece, size_t S, size_t stripes, void *stream) {
   if (c && c->w != 8) return fail(PMRC_EUNSUPPORTED, "w = 16 codes support encode, decode and repair (SURVEY NEXT-4)");
-  if (!c || !helper_ids || !betas) return fail(PMRC_EINVAL, "NULL argument");
+  if (!c || !helper_ids_in || !betas_in) return fail(PMRC_EINVAL, "NULL argument");
   int need = 0;
-  int rc = repair_common(c, lost_id, helper_ids, n_helpers, &need);
+  int rc = repair_common(c, lost_id, helper_ids_in, n_helpers, &need);
   if (rc) return rc;
+  std::vector<int> help_v;
+  std::vector<pmrc_cregion> b_v;
+  canonical_order(helper_ids_in, betas_in, n_helpers, help_v, b_v);
+  const int *helper_ids = help_v.data();
+  const pmrc_cregion *betas = b_v.data();
   if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
   const CodeDef &D = c->def;
   const std::string key = ids_key("comb", helper_ids, n_helpers, lost_id);

@@ -13,10 +13,11 @@
 //   * Instruction supply is the first-order constraint (profiles/r01): straight-line code that is
 //     not re-executed starves the SM.  So all warps of a CTA execute the same group at the same
 //     time, everything except the XOR networks is a loop, and per-group code stays ~20 KB.
-//   * Memory: each warp runs a 2-stage pipeline: while a stage computes, lane 0 issues TMA 1-D bulk
-//     copies (cp.async.bulk + mbarrier complete_tx) of the next stage's 1 KiB input blocks into the
-//     other shared-memory buffer.  Inputs that a later group reads again keep normal L2 priority;
-//     an input's last read and all parity stores carry an L2 evict-first policy.
+//   * Memory: each team of warps runs a 2-stage pipeline: while a stage computes, every lane issues
+//     16-B cp.async.cg copies (zero-fill via src-size at ragged ends) of the next stage's 1 KiB
+//     input blocks into the other shared-memory buffer.  (A lane-0 TMA 1-D bulk-copy variant with
+//     mbarrier complete_tx measured slower, profiles/r01/README.md v4 -> v5.)  Blocks read by a
+//     single group and all parity stores carry an L2 evict-first policy.
 //   * Each lane transposes its 32 bytes per block in place in shared memory (3 delta-swap stages,
 //     LOP3 mux + IMAD shifts) into 8 bit planes; the XOR network reads planes with LDS.128, keeps
 //     the group's 8 x 8 output planes in registers, then transposes back and stores 16-B vectors.
@@ -968,8 +969,7 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
             // producer: data landed -> transpose its share of the blocks -> FULL; wait until the
             // consumers released the other buffer (EMPTY) before loading the successor stage
             s << "          pm_cp_wait<0>();\n";
-            if (!(o.debug & 1))
-              s << "          pm_transpose_in(buf + lane * 16u, " << tsplit[si][rk] << "u, " << tsplit[si][rk + 1] << "u);\n";
+            s << "          pm_transpose_in(buf + lane * 16u, " << tsplit[si][rk] << "u, " << tsplit[si][rk + 1] << "u);\n";
             s << "          pm_team_arrive(4u * team + pb, PM_T * 32u);\n";
             s << "          if (kk != 0u" << (sj ? " || true" : "") << ") pm_team_sync(4u * team + 2u + (pb ^ 1u), PM_T * 32u);\n";
             prefetch(g, sj);
@@ -982,8 +982,7 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
         // consume: own copies landed -> transpose own share -> team barrier
         s << "          pm_cp_wait<" << (D - 1) << ">();\n";
         s << "          const u32 buf = sbuf + pb * (PM_QMAX * " << CB << "u);\n";
-        if (!(o.debug & 1))  // debug bit 0: skip the input transposes (timing experiments only: wrong results)
-          s << "          pm_transpose_in(buf + lane * 16u, " << tsplit[si][rk] << "u, " << tsplit[si][rk + 1] << "u);\n";
+        s << "          pm_transpose_in(buf + lane * 16u, " << tsplit[si][rk] << "u, " << tsplit[si][rk + 1] << "u);\n";
         s << "          const u32 pl = buf + lane * 16u;\n";
         }
         // the team barrier + the prefetch of the successor stage into the other buffer; emitted
@@ -1152,7 +1151,6 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
         const OutputDesc &od = p.outputs[G.rows[r0 + r]];
         std::string n = "o" + std::to_string(r);
         if (W == 8) {
-        if (!(o.debug & 2))  // debug bit 1: skip the output transposes (timing experiments only)
         s << "        pm_tr8(" << n << "_0, " << n << "_1, " << n << "_2, " << n << "_3, " << n << "_4, " << n << "_5, "
           << n << "_6, " << n << "_7);\n";
         s << "        { unsigned char *pp = (unsigned char *)(ob" << od.slot << " + (u64)" << od.blk << "u * S);\n";
@@ -1162,7 +1160,7 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
           s << "        { u32 wv[16] = {";
           for (int b = 0; b < 16; b++) s << (b ? ", " : "") << n << "_" << b;
           s << "};\n";
-          if (!(o.debug & 2)) s << "          pm_tr16(wv);\n";
+          s << "          pm_tr16(wv);\n";
           s << "          unsigned char *pp = (unsigned char *)(ob" << od.slot << " + (u64)" << od.blk << "u * S);\n";
           for (int q4 = 0; q4 < 4; q4++)
             s << "          pm_st(pp + o" << q4 << ", v" << q4 << ", wv[" << 4 * q4 << "], wv[" << 4 * q4 + 1 << "], wv["

@@ -80,7 +80,6 @@ struct GenOptions {
   int l2_shared = 0;        // layouts 1/2: L2 policy of blocks read by >1 group (-1 static last-read rule, 0 normal, 2 evict_last)
   int ws_prod = 1;          // producer warps per warp-specialised team
   bool ws = false;          // warp-specialised teams (producer transposes, consumers run networks)
-  int debug = 0;            // timing experiments only (wrong results): 1 skip input, 2 skip output transposes
   bool own_first = false;   // sub-networks over a warp's own transposed blocks before the team barrier
   int nbuf = 2;             // stage buffers per team (layouts 1/2): prefetch nbuf-1 stages ahead
   int tr_unroll = 1;        // unroll factor of the in-place input transpose loop

@@ -26,6 +26,11 @@ ENC_CASES = [
     (pm.PMRC_MSR_SPARSE, 16, 32, 1024 + 32, 1),
     (pm.PMRC_MSR_SPARSE, 2, 3, 16, 7),        # smallest code, one vector per block
     (pm.PMRC_MSR_SPARSE_N2K, 8, 16, 2048 + 32, 2),   # R15 extension
+    (pm.PMRC_MBR, 16, 32, 1024 + 16, 1),      # config 5's MBR k=16 plan (30 groups, 16-row groups, layout 0)
+    (pm.PMRC_MSR_SPARSE, 8, 16, (4 << 20) + 16, 1),   # config 5's largest sub-block (4 MiB), ragged
+    (pm.PMRC_MSR_VANILLA, 3, 6, 2048, 16),    # the k=3 codes the decode / repair tests start from
+    (pm.PMRC_MBR, 3, 6, 2048, 16),
+    (pm.PMRC_RS_VANDERMONDE, 3, 6, 2048, 16),
 ]
 
 
@@ -78,6 +83,8 @@ def test_decode_config1_every_subset(kind):
     st = Stripes(kind, k, n, S, stripes, seed=1)
     try:
         st.encode()
+        # the parity every decode starts from is itself the oracle's (not only self-consistent)
+        assert np.array_equal(st.parity.cpu().numpy(), O.encode(oracle_kind(kind), n, k, st.d, st.host_data()))
         for ids in itertools.combinations(range(n), k):
             out = torch.zeros_like(st.data)
             nw = pm.pmrc_decode(st.code, list(ids), [st.piece(i) for i in ids], out.data_ptr(), S, stripes, st.stream)
@@ -156,6 +163,7 @@ def test_repair_config1_every_node_every_helper_set(kind):
     st = Stripes(kind, k, n, S, stripes, seed=1)
     try:
         st.encode()
+        assert np.array_equal(st.parity.cpu().numpy(), O.encode(oracle_kind(kind), n, k, st.d, st.host_data()))
         d = st.d
         n_sing = 0
         for f in range(n):
@@ -262,10 +270,12 @@ def test_full_size_config2_sampled():
                 x = np.stack([inputs.host_bytes(W, 1234, t * B * S + c * S + p0, real) for c in range(B)])
                 want = O.encode(O.MSR_SPARSE, n, k, 14, x[None])[0]
                 assert np.array_equal(par[t, :, p0:p0 + W].cpu().numpy(), want), (t, p0)
-        # the padded tail of the last stripe is zero data, hence zero parity there
+        # R11: the last stripe holds the remaining 16 MiB of real data in its first 16 blocks and
+        # zero padding after them (its parity, which mixes both, is in the sampled windows above)
         last_real = real - (stripes - 1) * B * S
         full_blocks = last_real // S
-        assert not par[stripes - 1, :, :].any() if full_blocks == 0 else True
+        assert full_blocks == 16 and last_real % S == 0
+        assert data[stripes - 1, :full_blocks].any() and not data[stripes - 1, full_blocks:].any()
     finally:
         pm.pmrc_destroy(code)
 

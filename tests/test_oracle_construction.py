@@ -247,6 +247,22 @@ def test_validity_range_gf16_paper():
         assert O.validate16_sparse(k) == 0, k
 
 
+@pytest.mark.parametrize("k", [2, 3, 4, 5, 8, 12])
+def test_validity_gf16_negative_at_n2k(k):
+    # negative pin of the GF(2^16) validity check (a check that always answered "valid" would pass
+    # the test above): at n = 2k the sparse Psi's n - alpha = alpha + 2 Cauchy rows span only
+    # alpha + 1 dimensions (SURVEY §8(c) A7 -- a field-independent rank argument), so exactly the
+    # d-subsets that omit two identity rows (C(alpha, 2) of them, none for k = 2) are singular;
+    # at n = 2k - 1 (the paper's n = d + 1) none is.
+    from math import comb
+    alpha = k - 1
+    flags, sing = O.validate16_sparse_n(k, 2 * k)
+    assert sing == comb(alpha, 2)
+    assert bool(flags & 2) == (k >= 3)
+    flags1, sing1 = O.validate16_sparse_n(k, 2 * k - 1)
+    assert (flags1, sing1) == (0, 0) and O.validate16_sparse(k) == 0
+
+
 def test_gf16_field_vs_carryless():
     # the w = 16 field the check above uses: products equal carry-less multiplication reduced by
     # 0x1100B (independent reference), and g = 2 generates all 65,535 nonzero elements

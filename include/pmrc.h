@@ -153,6 +153,46 @@ int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids, int n_
 int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *in, size_t in_stride, void *out,
                size_t out_stride, size_t S, size_t stripes, void *stream);
 
+/* Engine policy.  Every call runs a plan (a coefficient matrix + its wiring) on one
+ * of two sm_100a kernels:
+ *   PMRC_PLAN_JIT      the plan's generated bitsliced kernel (GF(2) XOR network per coefficient
+ *                      matrix, zero coefficients skipped at generation time): the fastest
+ *                      for a hot pattern; the first use of a new pattern generates and NVRTC-
+ *                      compiles it (seconds) unless the in-tree kernel cache has it
+ *   PMRC_PLAN_RUNTIME  the precompiled runtime-coefficient kernel (PRMT 3-3-2 table lookups,
+ *                      coefficients as data): a new pattern costs only the host inversion and a
+ *                      table fill (P:216's per-pattern initialisation, well under a millisecond)
+ *   PMRC_PLAN_AUTO     (default) JIT for the encode (built at pmrc_create) and for plans whose JIT
+ *                      kernel is already loaded on the handle (pmrc_plan_prepare, or a call made
+ *                      under PMRC_PLAN_JIT); the runtime kernel for every other GF(2^8) plan.
+ * GF(2^16) codes always use JIT.  Results are bit-identical under every policy. */
+enum { PMRC_PLAN_AUTO = 0, PMRC_PLAN_JIT = 1, PMRC_PLAN_RUNTIME = 2 };
+int pmrc_set_plan_policy(pmrc_code *c, int policy);
+int pmrc_get_plan_policy(const pmrc_code *c);
+/* JIT-compile (or load from the kernel cache) and keep on the handle the generated kernel of a
+ * decode (op 0, ids = survivors) or repair (op 1, lost_id, ids = helpers) pattern, so that later
+ * calls with this pattern run it under PMRC_PLAN_AUTO (hot-pattern promotion).  Errors as
+ * pmrc_decode / pmrc_repair. */
+int pmrc_plan_prepare(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids);
+
+/* Per-stripe failure patterns in ONE launch (config 4 as BASELINE.json states it; the
+ * initialisation "depends on the failure pattern but can be reused across stripes"): stripe t has
+ * its own pattern, run by the runtime-coefficient kernel (GF(2^8) codes).  nodes[i] (i < n) is node
+ * i's piece region (stripe 0 + stripe stride, as pmrc_cregion elsewhere); only the regions a
+ * stripe's pattern reads are touched (and validated).  Patterns are cached on the handle by id set.
+ *
+ * decode: surv_ids[t * n_surv + q] = survivor q of stripe t (any order); data_out [stripes][B][S]
+ * receives, per stripe, the data blocks no surviving systematic node of that stripe holds (others
+ * untouched); n_written (may be NULL) receives stripes counts.  PMRC_ESINGULAR (detail names the
+ * stripe) if a stripe's survivors do not span the data. */
+int pmrc_decode_batch(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregion *nodes, void *data_out,
+                      size_t S, size_t stripes, int *n_written, void *stream);
+/* repair: lost_ids[t] and helper_ids[t * n_helpers + h] (n_helpers = d; RS: k) per stripe; out_piece
+ * receives stripe t's repaired piece (alpha blocks) at out_piece.ptr + t * stripe_stride.
+ * PMRC_ESINGULAR (detail names the stripe) for a singular (lost, helpers) pair (R10). */
+int pmrc_repair_batch(pmrc_code *c, const int *lost_ids, const int *helper_ids, int n_helpers, const pmrc_cregion *nodes,
+                      pmrc_region out_piece, size_t S, size_t stripes, void *stream);
+
 /* Cap the grid of every launch on this handle at max_ctas CTAs (0 = default: one full wave, one
  * persistent CTA per SM).  With a cap, small launches issued on several streams (e.g. config 4's
  * per-stripe failure patterns, one plan per stripe) run side by side on disjoint SMs instead of

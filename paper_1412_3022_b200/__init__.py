@@ -16,13 +16,16 @@ PMRC_MSR_SPARSE, PMRC_MSR_VANILLA, PMRC_MBR, PMRC_RS_VANDERMONDE, PMRC_MSR_SPARS
 PMRC_OK, PMRC_EINVAL, PMRC_EUNSUPPORTED, PMRC_ESINGULAR = 0, -1, -2, -3
 PMRC_EALIGN, PMRC_ENOMEM, PMRC_ECUDA, PMRC_EJIT = -4, -5, -6, -7
 
+PMRC_PLAN_AUTO, PMRC_PLAN_JIT, PMRC_PLAN_RUNTIME = 0, 1, 2
+
 MATRIX_PSI, MATRIX_G, MATRIX_GSYS, MATRIX_GPP, MATRIX_LAMBDA, MATRIX_GTINV = 0, 1, 2, 3, 4, 5
 
 EXPORTS = ["pmrc_create", "pmrc_destroy", "pmrc_info", "pmrc_matrix", "pmrc_layout", "pmrc_encode",
            "pmrc_encode_host", "pmrc_decode", "pmrc_repair", "pmrc_repair_project", "pmrc_repair_combine",
            "pmrc_read_cost", "pmrc_launch_count", "pmrc_strerror", "pmrc_last_error", "pmrc_precompile",
            "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source", "pmrc_plan_stats", "pmrc_apply", "pmrc_apply_stats", "pmrc_set_max_ctas",
-           "pmrc_set_independent_launches"]
+           "pmrc_set_independent_launches", "pmrc_set_plan_policy", "pmrc_get_plan_policy", "pmrc_plan_prepare",
+           "pmrc_decode_batch", "pmrc_repair_batch"]
 
 
 class PmrcError(RuntimeError):
@@ -89,6 +92,11 @@ def lib():
             "pmrc_apply_stats": ([P, P, I, I, ctypes.POINTER(pmrc_plan_stats_t)], I),
             "pmrc_set_max_ctas": ([P, I], I),
             "pmrc_set_independent_launches": ([P, I], I),
+            "pmrc_set_plan_policy": ([P, I], I),
+            "pmrc_get_plan_policy": ([P], I),
+            "pmrc_plan_prepare": ([P, I, I, IP, I], I),
+            "pmrc_decode_batch": ([P, IP, I, ctypes.POINTER(pmrc_cregion), P, Z, Z, IP, P], I),
+            "pmrc_repair_batch": ([P, IP, IP, I, ctypes.POINTER(pmrc_cregion), pmrc_region, Z, Z, P], I),
             "pmrc_strerror": ([I], ctypes.c_char_p),
             "pmrc_last_error": ([], ctypes.c_char_p),
         }
@@ -234,6 +242,47 @@ def pmrc_set_max_ctas(code, max_ctas):
 def pmrc_set_independent_launches(code, on):
     """Declare consecutive launches of this handle independent (programmatic dependent launch)."""
     _check(lib().pmrc_set_independent_launches(code, int(on)), "pmrc_set_independent_launches")
+
+
+def pmrc_set_plan_policy(code, policy):
+    """PMRC_PLAN_AUTO (default), PMRC_PLAN_JIT or PMRC_PLAN_RUNTIME (include/pmrc.h)."""
+    _check(lib().pmrc_set_plan_policy(code, int(policy)), "pmrc_set_plan_policy")
+
+
+def pmrc_get_plan_policy(code):
+    return int(lib().pmrc_get_plan_policy(code))
+
+
+def pmrc_plan_prepare(code, op, lost_id, ids):
+    """JIT-compile and keep the generated kernel of a decode (op 0) / repair (op 1) pattern."""
+    arr, n = _ints(ids)
+    _check(lib().pmrc_plan_prepare(code, op, lost_id, arr, n), "pmrc_plan_prepare")
+
+
+def pmrc_decode_batch(code, surv_ids, nodes, data_out_ptr, S, stripes, stream=0):
+    """surv_ids: stripes x n_surv survivor ids (per stripe); nodes: n (ptr, stripe_stride) piece
+    regions, one per node.  Returns the list of blocks written per stripe."""
+    rows = [list(r) for r in surv_ids]
+    n_surv = len(rows[0]) if rows else 0
+    assert len(rows) == stripes and all(len(r) == n_surv for r in rows)
+    ids, _ = _ints([x for r in rows for x in r])
+    regs = (pmrc_cregion * max(1, len(nodes)))(*[pmrc_cregion(p, s) for p, s in nodes])
+    nw = (ctypes.c_int * max(1, stripes))()
+    _check(lib().pmrc_decode_batch(code, ids, n_surv, regs, data_out_ptr, S, stripes, nw, stream), "pmrc_decode_batch")
+    return list(nw[:stripes])
+
+
+def pmrc_repair_batch(code, lost_ids, helper_ids, nodes, out_piece, S, stripes, stream=0):
+    """lost_ids: per stripe; helper_ids: stripes x d; nodes: n (ptr, stripe_stride) piece regions;
+    out_piece: (ptr, stripe_stride) of the repaired pieces."""
+    rows = [list(r) for r in helper_ids]
+    nh = len(rows[0]) if rows else 0
+    assert len(rows) == stripes == len(lost_ids) and all(len(r) == nh for r in rows)
+    lost, _ = _ints(lost_ids)
+    ids, _ = _ints([x for r in rows for x in r])
+    regs = (pmrc_cregion * max(1, len(nodes)))(*[pmrc_cregion(p, s) for p, s in nodes])
+    _check(lib().pmrc_repair_batch(code, lost, ids, nh, regs, pmrc_region(*out_piece), S, stripes, stream),
+           "pmrc_repair_batch")
 
 
 def pmrc_apply_stats(code, A):

@@ -13,7 +13,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
-HOST_SRC = ["gf256.cpp", "construct.cpp", "xorprog.cpp", "codegen.cpp", "plan.cpp", "cudrv.cpp", "capi.cpp"]
+HOST_SRC = ["gf256.cpp", "construct.cpp", "xorprog.cpp", "codegen.cpp", "plan.cpp", "cudrv.cpp", "rtplan.cpp",
+            "capi.cpp"]
+RT_SRC = ["rlc.cu"]   # hand-written sm_100a kernels compiled by nvcc into libpmrc.so
 LIB = os.path.join(HERE, "libpmrc.so")
 INPUTS_LIB = os.path.join(ROOT, "inputs", "libpmrc_inputs.so")
 NVCC_ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -36,11 +38,20 @@ def _stale(target, sources):
 
 def build_lib(force=False):
     srcs = [os.path.join(HERE, "csrc", "host", s) for s in HOST_SRC]
-    deps = srcs + [os.path.join(HERE, "csrc", "host", h) for h in os.listdir(os.path.join(HERE, "csrc", "host"))
-                   if h.endswith(".hpp")] + [os.path.join(ROOT, "include", "pmrc.h")]
+    rt = [os.path.join(HERE, "csrc", "rt", s) for s in RT_SRC]
+    hdrs = [os.path.join(HERE, "csrc", d, h) for d in ("host", "rt") for h in os.listdir(os.path.join(HERE, "csrc", d))
+            if h.endswith(".hpp")]
+    deps = srcs + rt + hdrs + [os.path.join(ROOT, "include", "pmrc.h")]
     if force or _stale(LIB, deps):
+        objs = []
+        for cu in rt:
+            obj = os.path.join(HERE, "csrc", "rt", os.path.basename(cu)[:-3] + ".o")
+            _run([os.path.join(CUDA, "bin", "nvcc")] + NVCC_ARCH +
+                 ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
+                  "-c", "-o", obj, cu])
+            objs.append(obj)
         _run(["g++", "-O2", "-g", "-std=c++17", "-fPIC", "-shared", "-Wall", "-Wno-unused-function",
-              "-I" + os.path.join(CUDA, "include"), "-o", LIB] + srcs +
+              "-I" + os.path.join(CUDA, "include"), "-o", LIB] + srcs + objs +
              ["-L" + os.path.join(CUDA, "lib64"), "-lnvrtc", "-lcudart", "-ldl", "-lpthread",
               "-Wl,-rpath," + os.path.join(CUDA, "lib64")])
     return LIB

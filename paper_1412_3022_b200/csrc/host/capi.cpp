@@ -12,8 +12,10 @@
 #include <vector>
 
 #include "../../../include/pmrc.h"
+#include "../rt/rlc.hpp"
 #include "construct.hpp"
 #include "plan.hpp"
+#include "rtplan.hpp"
 
 using namespace pmrc;
 
@@ -56,6 +58,9 @@ struct pmrc_code {
   PlanSpec dry_spec;           //   and the plan
   GenStats dry_stats;
   bool dry_compile = false;    //   (and NVRTC-compiles it into the kernel cache if set)
+  int policy = PMRC_PLAN_AUTO; // engine choice (pmrc_set_plan_policy)
+  std::map<std::string, std::unique_ptr<PlanSpec>> specs;  // plan specs by key (null: nothing to compute)
+  std::map<std::string, std::unique_ptr<RtPlan>> rt_plans; // runtime-coefficient plans by key + shape
 };
 
 namespace {
@@ -244,6 +249,7 @@ int apply_gen_knobs(const std::string &s, GenOptions &G, std::string &err) {
       {"ws", 0, [](GenOptions &o, int v) { o.ws = v != 0; }},
       {"ws_prod", 1, [](GenOptions &o, int v) { o.ws_prod = v; }},
       {"grid_ctas", 1, [](GenOptions &o, int v) { o.grid_ctas = v; }},
+      {"rt_groups", 0, [](GenOptions &o, int v) { o.rt_groups = v; }},
   };
   std::string applied;
   size_t pos = 0;
@@ -280,6 +286,8 @@ int apply_gen_knobs(const std::string &s, GenOptions &G, std::string &err) {
 }
 
 }  // namespace
+
+static int get_rt_plan(pmrc_code *c, const std::string &key, const PlanSpec &spec, int R, RtPlan **out);
 
 extern "C" {
 
@@ -364,6 +372,7 @@ void pmrc_destroy(pmrc_code *c) {
   if (c->device >= 0 && have) cudaSetDevice(c->device);
   free_kernel(c->enc);
   for (auto &kv : c->plans) free_kernel(*kv.second);
+  for (auto &kv : c->rt_plans) rt_free(*kv.second);
   for (int i = 0; i < kHostBufs; i++) {
     if (c->hs.d_data[i]) cudaFree(c->hs.d_data[i]);
     if (c->hs.d_par[i]) cudaFree(c->hs.d_par[i]);
@@ -546,11 +555,23 @@ int pmrc_encode(pmrc_code *c, const void *data, void *parity, size_t S, size_t s
   int rc = check_region(data, (size_t)D.B * S, stripes);
   if (!rc) rc = check_region(parity, (size_t)D.P * S, stripes);
   if (rc) return fail(rc, "bad data/parity pointer");
-  rc = build_encode(c);
-  if (rc) return rc;
   uint64_t ptrs[2] = {(uint64_t)(uintptr_t)data, (uint64_t)(uintptr_t)parity};
   uint64_t strides[2] = {(uint64_t)D.B * S, (uint64_t)D.P * S};
   std::string err;
+  if (c->policy == PMRC_PLAN_RUNTIME && c->w == 8) {
+    // the same G'' on the runtime-coefficient kernel (the formulation comparison of DESIGN.md)
+    const pmrc_rt::RlcShape sh = rt_shape(D.P, c->gen);
+    RtPlan *P = nullptr;
+    rc = get_rt_plan(c, "enc", c->enc_spec, sh.R, &P);
+    if (rc) return rc;
+    rc = ensure_device(c);
+    if (rc) return rc;
+    rc = rt_launch({P}, nullptr, ptrs, strides, 2, S, stripes, sh, stream, c->max_ctas, err);
+    if (rc) return fail(rc, err);
+    return PMRC_OK;
+  }
+  rc = build_encode(c);
+  if (rc) return rc;
   if (c->enc.pace) c->traced = &c->enc;
   rc = launch_kernel(c->enc, ptrs, strides, S, stripes, stream, err, c->max_ctas);
   if (rc) return fail(rc, err);
@@ -624,11 +645,20 @@ int pmrc_encode_host(pmrc_code *c, const void *data_host, void *parity_host, siz
   return PMRC_OK;
 }
 
-// GF(2^16) decode plan (w = 16): the same rule as the GF(2^8) plan in pmrc_decode (R13):
-// greedy B independent rows of G' = [I_B; G''], systematic survivors first, then the inverse's
-// rows of the data blocks no surviving systematic node holds.  Returns 0, PMRC_ESINGULAR, or 1 if
-// nothing is missing.
-static int decode_spec16(const pmrc_code *c, const int *surv_ids, int n_surv, PlanSpec &spec) {
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// Plan specs of decode and repair.  slot_of[q] is the slot that survivor / helper q's piece is
+// read from (single calls: q; batch calls: the node id), out_slot the output region's slot.
+// Each returns PMRC_OK, PMRC_ESINGULAR, or kNothing (no block to compute).
+// ---------------------------------------------------------------------------------------------
+constexpr int kNothing = 1;
+
+// GF(2^16) decode plan (w = 16): the same rule as the GF(2^8) plan (R13): greedy B
+// independent rows of G' = [I_B; G''], systematic survivors first, then the inverse's rows of the
+// data blocks no surviving systematic node holds.
+static int decode_spec16(const pmrc_code *c, const int *surv_ids, int n_surv, const int *slot_of, int out_slot,
+                         int n_slots, PlanSpec &spec) {
   const CodeDef &D = c->def;
   const GF65536 &F = gf16();
   const int B = D.B, a = D.alpha;
@@ -712,17 +742,17 @@ static int decode_spec16(const pmrc_code *c, const int *surv_ids, int n_surv, Pl
   std::vector<int> missing, used;
   for (int x = 0; x < B; x++)
     if (!held[x]) missing.push_back(x);
-  if (missing.empty()) return 1;
+  if (missing.empty()) return kNothing;
   for (int x = 0; x < B; x++) {
     bool nz = false;
     for (int m : missing) nz |= Inv[(size_t)m * B + x] != 0;
     if (nz) used.push_back(x);
   }
   spec = PlanSpec();
-  spec.n_slots = n_surv + 1;
+  spec.n_slots = n_slots;
   spec.w = 16;
-  for (int x : used) spec.inputs.push_back({{{sel[x].first, sel[x].second, 1}}});
-  for (int m : missing) spec.outputs.push_back({n_surv, m});
+  for (int x : used) spec.inputs.push_back({{{slot_of[sel[x].first], sel[x].second, 1}}});
+  for (int m : missing) spec.outputs.push_back({out_slot, m});
   spec.A = Mat((int)missing.size(), (int)used.size());
   spec.A16.assign(missing.size() * used.size(), 0);
   for (size_t r = 0; r < missing.size(); r++)
@@ -734,139 +764,298 @@ static int decode_spec16(const pmrc_code *c, const int *surv_ids, int n_surv, Pl
   return PMRC_OK;
 }
 
+// GF(2^8) decode plan (R13): greedy B independent rows of G', systematic survivors
+// first, then ascending id; invert; keep the rows of the data blocks no surviving systematic node
+// holds, over the columns they use (the lazy decode of P:106: only missing blocks are computed).
+static int decode_spec8(const pmrc_code *c, const int *surv_ids, int n_surv, const int *slot_of, int out_slot,
+                        int n_slots, PlanSpec &spec) {
+  const CodeDef &D = c->def;
+  std::vector<int> order;
+  for (int pass = 0; pass < 2; pass++)
+    for (int id = 0; id < D.n; id++) {
+      if ((pass == 0) != (id < D.k)) continue;
+      for (int a = 0; a < n_surv; a++)
+        if (surv_ids[a] == id) order.push_back(a);
+    }
+  std::vector<std::vector<uint8_t>> basis;  // reduced rows (incremental elimination)
+  std::vector<int> pivcol;
+  std::vector<std::pair<int, int>> sel;  // (survivor index, symbol)
+  Mat Sel(D.B, D.B);
+  const GF256 &F = gf();
+  for (int a : order) {
+    for (int j = 0; j < D.alpha && (int)sel.size() < D.B; j++) {
+      std::vector<uint8_t> row(D.B);
+      for (int x = 0; x < D.B; x++) row[x] = D.Gsys.at(surv_ids[a] * D.alpha + j, x);
+      std::vector<uint8_t> red = row;
+      for (size_t bi = 0; bi < basis.size(); bi++) {
+        uint8_t f = red[pivcol[bi]];
+        if (!f) continue;
+        for (int x = 0; x < D.B; x++) red[x] ^= F.mul(f, basis[bi][x]);
+      }
+      int pc = -1;
+      for (int x = 0; x < D.B; x++)
+        if (red[x]) { pc = x; break; }
+      if (pc < 0) continue;
+      uint8_t s = F.inv(red[pc]);
+      for (int x = 0; x < D.B; x++) red[x] = F.mul(red[x], s);
+      for (size_t bi = 0; bi < basis.size(); bi++) {
+        uint8_t f = basis[bi][pc];
+        if (!f) continue;
+        for (int x = 0; x < D.B; x++) basis[bi][x] ^= F.mul(f, red[x]);
+      }
+      basis.push_back(red);
+      pivcol.push_back(pc);
+      for (int x = 0; x < D.B; x++) Sel.at((int)sel.size(), x) = row[x];
+      sel.push_back({a, j});
+    }
+  }
+  if ((int)sel.size() < D.B) return PMRC_ESINGULAR;
+  Mat Inv;
+  if (!invert(Sel, Inv)) return PMRC_ESINGULAR;
+  std::vector<char> held(D.B, 0);
+  for (int a = 0; a < n_surv; a++)
+    if (surv_ids[a] < D.k)
+      for (int j = 0; j < D.alpha; j++) held[D.sys_block(surv_ids[a], j)] = 1;
+  std::vector<int> missing;
+  for (int x = 0; x < D.B; x++)
+    if (!held[x]) missing.push_back(x);
+  if (missing.empty()) return kNothing;
+  spec = PlanSpec();
+  spec.n_slots = n_slots;
+  std::vector<int> used_cols;
+  for (int x = 0; x < D.B; x++) {
+    bool nz = false;
+    for (int m : missing) nz |= Inv.at(m, x) != 0;
+    if (nz) used_cols.push_back(x);
+  }
+  for (int x : used_cols) spec.inputs.push_back({{{slot_of[sel[x].first], sel[x].second, 1}}});
+  for (int m : missing) spec.outputs.push_back({out_slot, m});
+  spec.A = Mat((int)missing.size(), (int)used_cols.size());
+  for (size_t r = 0; r < missing.size(); r++)
+    for (size_t x = 0; x < used_cols.size(); x++) spec.A.at((int)r, (int)x) = Inv.at(missing[r], used_cols[x]);
+  return PMRC_OK;
+}
+
+static int decode_spec(const pmrc_code *c, const int *surv, int n_surv, const int *slot_of, int out_slot, int n_slots,
+                       PlanSpec &spec) {
+  return c->w == 16 ? decode_spec16(c, surv, n_surv, slot_of, out_slot, n_slots, spec)
+                    : decode_spec8(c, surv, n_surv, slot_of, out_slot, n_slots, spec);
+}
+
+// Fused repair plan (P:53 footnote): input h = beta_h = mu . piece_h (derived; only
+// the blocks with a nonzero mu are read), outputs = the alpha blocks of the lost piece,
+// A = R (the newcomer's matrix: MSR [I | lambda_f I] Psi_H^{-1}, MBR Psi_H^{-1}, RS G'_f (G'_H)^{-1}).
+static int repair_spec(const pmrc_code *c, int f, const int *H, int nh, const int *slot_of, int out_slot, int n_slots,
+                       PlanSpec &spec) {
+  const CodeDef &D = c->def;
+  spec = PlanSpec();
+  spec.n_slots = n_slots;
+  if (c->w == 16) {
+    const GF65536 &F = gf16();
+    const int dd = D.d, a = D.alpha;
+    std::vector<uint16_t> Wm((size_t)dd * dd), Inv((size_t)dd * dd, 0);
+    for (int r = 0; r < dd; r++) {
+      for (int x = 0; x < dd; x++) Wm[(size_t)r * dd + x] = c->psi16[(size_t)H[r] * dd + x];
+      Inv[(size_t)r * dd + r] = 1;
+    }
+    for (int col = 0; col < dd; col++) {
+      int piv = -1;
+      for (int r = col; r < dd; r++)
+        if (Wm[(size_t)r * dd + col]) { piv = r; break; }
+      if (piv < 0) return PMRC_ESINGULAR;
+      if (piv != col)
+        for (int x = 0; x < dd; x++) {
+          std::swap(Wm[(size_t)piv * dd + x], Wm[(size_t)col * dd + x]);
+          std::swap(Inv[(size_t)piv * dd + x], Inv[(size_t)col * dd + x]);
+        }
+      const uint16_t sc = F.inv(Wm[(size_t)col * dd + col]);
+      for (int x = 0; x < dd; x++) {
+        Wm[(size_t)col * dd + x] = F.mul(Wm[(size_t)col * dd + x], sc);
+        Inv[(size_t)col * dd + x] = F.mul(Inv[(size_t)col * dd + x], sc);
+      }
+      for (int r = 0; r < dd; r++) {
+        const uint16_t g = r == col ? 0 : Wm[(size_t)r * dd + col];
+        if (!g) continue;
+        for (int x = 0; x < dd; x++) {
+          Wm[(size_t)r * dd + x] ^= F.mul(g, Wm[(size_t)col * dd + x]);
+          Inv[(size_t)r * dd + x] ^= F.mul(g, Inv[(size_t)col * dd + x]);
+        }
+      }
+    }
+    const uint16_t lf = c->lam16[f];
+    spec.w = 16;
+    for (int h = 0; h < nh; h++) {
+      InputDesc in;
+      for (int b = 0; b < a; b++) {
+        const uint16_t mu = c->psi16[(size_t)f * dd + b];
+        if (mu) in.terms.push_back({slot_of[h], b, mu});
+      }
+      spec.inputs.push_back(in);
+    }
+    for (int q = 0; q < a; q++) spec.outputs.push_back({out_slot, q});
+    spec.A = Mat(a, nh);
+    spec.A16.assign((size_t)a * nh, 0);
+    for (int q = 0; q < a; q++)
+      for (int h = 0; h < nh; h++) {
+        const uint16_t v = Inv[(size_t)q * dd + h] ^ F.mul(lf, Inv[(size_t)(a + q) * dd + h]);
+        spec.A16[(size_t)q * nh + h] = v;
+        spec.A.at(q, h) = v ? 1 : 0;
+      }
+    return PMRC_OK;
+  }
+  Mat R;
+  if (!repair_matrix(D, f, H, R)) return PMRC_ESINGULAR;  // R10: predicted singular sets at n >= 2k
+  std::vector<uint8_t> mu = repair_mu(D, f);
+  for (int h = 0; h < nh; h++) {
+    InputDesc in;
+    for (size_t b = 0; b < mu.size(); b++)
+      if (mu[b]) in.terms.push_back({slot_of[h], (int)b, mu[b]});
+    spec.inputs.push_back(in);
+  }
+  for (int a = 0; a < D.alpha; a++) spec.outputs.push_back({out_slot, a});
+  spec.A = R;
+  return PMRC_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Engines.  Every data-path call runs a plan on one of two kernels:
+//   JIT      the generated bitsliced kernel of the plan (codegen.cpp; NVRTC on first use unless
+//            the in-tree cache has it): the fastest, but the first contact with a new failure
+//            pattern costs kernel generation + NVRTC (seconds)
+//   RUNTIME  the precompiled runtime-coefficient kernel (csrc/rt/rlc.cu): coefficients are data,
+//            a new pattern costs the host inversion + table fill (P:216's initialisation)
+// Policy PMRC_PLAN_AUTO (default): JIT for the encode (compiled at pmrc_create) and for plans whose
+// JIT kernel is already loaded on the handle (pmrc_plan_prepare / earlier JIT calls), RUNTIME for
+// every other plan; GF(2^16) plans always use JIT.
+// ---------------------------------------------------------------------------------------------
+static bool use_runtime(const pmrc_code *c, const std::string &key) {
+  if (c->w != 8) return false;
+  if (c->policy == PMRC_PLAN_JIT) return false;
+  if (c->policy == PMRC_PLAN_RUNTIME) return true;
+  return !c->plans.count(key);
+}
+
+static std::string rt_key(const std::string &key, int R) { return key + "#rt" + std::to_string(R); }
+
+// runtime plan of `spec` for R-row blocks, cached on the handle under `key`
+static int get_rt_plan(pmrc_code *c, const std::string &key, const PlanSpec &spec, int R, RtPlan **out) {
+  const std::string k = rt_key(key, R);
+  auto it = c->rt_plans.find(k);
+  if (it != c->rt_plans.end()) {
+    *out = it->second.get();
+    return PMRC_OK;
+  }
+  auto p = std::make_unique<RtPlan>();
+  std::string err;
+  int rc = rt_build(spec, R, *p, err);
+  if (rc) return fail(rc, err);
+  *out = p.get();
+  c->rt_plans[k] = std::move(p);
+  return PMRC_OK;
+}
+
+// The plan cache: key -> spec (built once; nullptr-equivalent when the plan computes nothing),
+// cached failures (ESINGULAR) in plan_err, number of outputs in plan_meta.
+template <class Make>
+static int get_spec(pmrc_code *c, const std::string &key, Make make, const PlanSpec **out) {
+  *out = nullptr;
+  auto fe = c->plan_err.find(key);
+  if (fe != c->plan_err.end())
+    return fail(fe->second, fe->second == PMRC_ESINGULAR ? "singular (cached): survivors do not span the data / "
+                                                           "Psi_H singular (DESIGN.md R10)"
+                                                         : "plan failed (cached)");
+  auto it = c->specs.find(key);
+  if (it == c->specs.end() || c->dry) {
+    auto sp = std::make_unique<PlanSpec>();
+    const int rc = make(*sp);
+    if (rc == PMRC_ESINGULAR) {
+      c->plan_err[key] = rc;
+      return fail(rc, "singular: survivors do not span the data / Psi_H singular for this (lost, helpers) pair "
+                      "(DESIGN.md R10)");
+    }
+    if (rc && rc != kNothing) return rc;
+    c->plan_meta[key] = rc == kNothing ? 0 : (int)sp->outputs.size();
+    if (rc == kNothing) sp.reset();
+    it = c->specs.insert_or_assign(key, std::move(sp)).first;
+  }
+  *out = it->second.get();
+  return PMRC_OK;
+}
+
+// Run a single plan over `stripes` stripes (slots of stripe 0 in ptrs, their strides).
+static int run_plan(pmrc_code *c, const std::string &key, const PlanSpec &spec, const uint64_t *ptrs,
+                    const uint64_t *strides, size_t S, size_t stripes, void *stream) {
+  std::string err;
+  if (c->dry) {
+    Kernel *K = nullptr;
+    return get_kernel(c, key, spec, &K);  // kDryRun (source / stats only)
+  }
+  if (use_runtime(c, key)) {
+    const pmrc_rt::RlcShape sh = rt_shape((int)spec.outputs.size(), c->gen);
+    RtPlan *P = nullptr;
+    int rc = get_rt_plan(c, key, spec, sh.R, &P);
+    if (rc == PMRC_OK) {
+      if (!stripes || !S) return PMRC_OK;
+      rc = ensure_device(c);
+      if (rc) return rc;
+      rc = rt_launch({P}, nullptr, ptrs, strides, spec.n_slots, S, stripes, sh, stream, c->max_ctas, err);
+      if (rc) return fail(rc, err);
+      return PMRC_OK;
+    }
+    if (!(rc == PMRC_EUNSUPPORTED && c->policy == PMRC_PLAN_AUTO)) return rc;
+    // AUTO: plans the runtime kernel cannot hold (tables above its shared-memory budget) use JIT
+  }
+  Kernel *K = nullptr;
+  int rc = get_kernel(c, key, spec, &K);
+  if (rc) return rc;
+  if (!stripes || !S) return PMRC_OK;
+  if (K->pace) c->traced = K;
+  rc = launch_kernel(*K, ptrs, strides, S, stripes, stream, err, c->max_ctas);
+  if (rc) return fail(rc, err);
+  return PMRC_OK;
+}
+
+extern "C" {
+
 int pmrc_decode(pmrc_code *c, const int *surv_ids_in, int n_surv, const pmrc_cregion *pieces_in, void *data_out,
                 size_t S, size_t stripes, int *n_written, void *stream) {
   if (n_written) *n_written = 0;
   if (!c || !surv_ids_in || !pieces_in || !data_out) return fail(PMRC_EINVAL, "NULL argument");
   const CodeDef &D = c->def;
   if (n_surv < 1 || n_surv > D.n || check_ids(D, surv_ids_in, n_surv)) return fail(PMRC_EINVAL, "bad survivor ids");
+  if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
   // canonical order: the plan (and its cache key) depends on the survivor SET only; the pieces are
   // permuted with the ids (the decoded data is unique, so the order cannot change it)
-  std::vector<int> surv_v;
-  std::vector<pmrc_cregion> pieces_v;
-  canonical_order(surv_ids_in, pieces_in, n_surv, surv_v, pieces_v);
-  const int *surv_ids = surv_v.data();
-  const pmrc_cregion *pieces = pieces_v.data();
-  if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
-  const std::string key = ids_key("dec", surv_ids, n_surv, 0);
-  auto fe = c->plan_err.find(key);
-  if (fe != c->plan_err.end()) return fail(fe->second, "survivors do not span the data (cached)");
-  if (c->w == 16 && (c->dry || !c->plan_meta.count(key))) {
-    PlanSpec spec;
-    const int r16 = decode_spec16(c, surv_ids, n_surv, spec);
-    if (r16 == PMRC_ESINGULAR) {
-      c->plan_err[key] = PMRC_ESINGULAR;
-      return fail(PMRC_ESINGULAR, "survivors do not span the data");
-    }
-    if (r16 == 1) {
-      c->plan_meta[key] = 0;
-      return PMRC_OK;
-    }
-    Kernel *Kb = nullptr;
-    int rc = get_kernel(c, key, spec, &Kb);
-    if (rc) return rc;
-    c->plan_meta[key] = (int)spec.outputs.size();
-  } else if (c->dry || !c->plan_meta.count(key)) {
-    PlanSpec spec;
-    {
-      // ---- plan (R13): greedy B independent rows of G', systematic survivors first ----
-      std::vector<int> order;
-      for (int pass = 0; pass < 2; pass++)
-        for (int id = 0; id < D.n; id++) {
-          if ((pass == 0) != (id < D.k)) continue;
-          for (int a = 0; a < n_surv; a++)
-            if (surv_ids[a] == id) order.push_back(a);
-        }
-      // incremental elimination to test independence
-      std::vector<std::vector<uint8_t>> basis;  // reduced rows
-      std::vector<int> pivcol;
-      std::vector<std::pair<int, int>> sel;  // (survivor index, symbol)
-      Mat Sel(D.B, D.B);
-      const GF256 &F = gf();
-      for (int a : order) {
-        for (int j = 0; j < D.alpha && (int)sel.size() < D.B; j++) {
-          std::vector<uint8_t> row(D.B);
-          for (int x = 0; x < D.B; x++) row[x] = D.Gsys.at(surv_ids[a] * D.alpha + j, x);
-          std::vector<uint8_t> red = row;
-          for (size_t bi = 0; bi < basis.size(); bi++) {
-            uint8_t f = red[pivcol[bi]];
-            if (!f) continue;
-            for (int x = 0; x < D.B; x++) red[x] ^= F.mul(f, basis[bi][x]);
-          }
-          int pc = -1;
-          for (int x = 0; x < D.B; x++)
-            if (red[x]) { pc = x; break; }
-          if (pc < 0) continue;
-          uint8_t s = F.inv(red[pc]);
-          for (int x = 0; x < D.B; x++) red[x] = F.mul(red[x], s);
-          // keep basis fully reduced on pivot columns
-          for (size_t bi = 0; bi < basis.size(); bi++) {
-            uint8_t f = basis[bi][pc];
-            if (!f) continue;
-            for (int x = 0; x < D.B; x++) basis[bi][x] ^= F.mul(f, red[x]);
-          }
-          basis.push_back(red);
-          pivcol.push_back(pc);
-          for (int x = 0; x < D.B; x++) Sel.at((int)sel.size(), x) = row[x];
-          sel.push_back({a, j});
-        }
-      }
-      if ((int)sel.size() < D.B) {
-        c->plan_err[key] = PMRC_ESINGULAR;
-        return fail(PMRC_ESINGULAR, "survivors do not span the data");
-      }
-      Mat Inv;
-      if (!invert(Sel, Inv)) return fail(PMRC_ESINGULAR, "selected rows singular");
-      // missing data blocks: not held by a surviving systematic node
-      std::vector<char> held(D.B, 0);
-      for (int a = 0; a < n_surv; a++)
-        if (surv_ids[a] < D.k)
-          for (int j = 0; j < D.alpha; j++) held[D.sys_block(surv_ids[a], j)] = 1;
-      std::vector<int> missing;
-      for (int x = 0; x < D.B; x++)
-        if (!held[x]) missing.push_back(x);
-      if (missing.empty()) {
-        c->plan_meta[key] = 0;
-        return PMRC_OK;
-      }
-      spec.n_slots = n_surv + 1;
-      std::vector<int> used_cols;
-      for (int x = 0; x < D.B; x++) {
-        bool nz = false;
-        for (int m : missing) nz |= Inv.at(m, x) != 0;
-        if (nz) used_cols.push_back(x);
-      }
-      for (int x : used_cols) spec.inputs.push_back({{{sel[x].first, sel[x].second, 1}}});
-      for (int m : missing) spec.outputs.push_back({n_surv, m});
-      spec.A = Mat((int)missing.size(), (int)used_cols.size());
-      for (size_t r = 0; r < missing.size(); r++)
-        for (size_t x = 0; x < used_cols.size(); x++) spec.A.at((int)r, (int)x) = Inv.at(missing[r], used_cols[x]);
-    }
-    Kernel *Kb = nullptr;
-    int rc = get_kernel(c, key, spec, &Kb);
-    if (rc) return rc;
-    c->plan_meta[key] = (int)spec.outputs.size();
-  }
+  std::vector<int> surv;
+  std::vector<pmrc_cregion> pieces;
+  canonical_order(surv_ids_in, pieces_in, n_surv, surv, pieces);
+  const std::string key = ids_key("dec", surv.data(), n_surv, 0);
+  std::vector<int> slot_of(n_surv);
+  for (int q = 0; q < n_surv; q++) slot_of[q] = q;
+  const PlanSpec *spec = nullptr;
+  int rc = get_spec(c, key, [&](PlanSpec &sp) { return decode_spec(c, surv.data(), n_surv, slot_of.data(), n_surv,
+                                                                    n_surv + 1, sp); },
+                    &spec);
+  if (rc) return rc;
   const int written = c->plan_meta[key];
-  Kernel *K = written ? c->plans[key].get() : nullptr;
   if (n_written) *n_written = written;
-  if (!written || !stripes || !S) return PMRC_OK;
+  if (!spec) return PMRC_OK;  // every data block survives on a systematic node
   std::vector<uint64_t> ptrs(n_surv + 1), strides(n_surv + 1);
+  if (!c->dry && stripes && S) {
+    for (int a = 0; a < n_surv; a++) {
+      rc = check_region(pieces[a].ptr, pieces[a].stripe_stride, stripes);
+      if (rc) return fail(rc, "bad survivor piece region");
+    }
+    rc = check_region(data_out, (size_t)D.B * S, stripes);
+    if (rc) return fail(rc, "bad data_out");
+  }
   for (int a = 0; a < n_surv; a++) {
-    int rc = check_region(pieces[a].ptr, pieces[a].stripe_stride, stripes);
-    if (rc) return fail(rc, "bad survivor piece region");
     ptrs[a] = (uint64_t)(uintptr_t)pieces[a].ptr;
     strides[a] = pieces[a].stripe_stride;
   }
-  int rc = check_region(data_out, (size_t)D.B * S, stripes);
-  if (rc) return fail(rc, "bad data_out");
   ptrs[n_surv] = (uint64_t)(uintptr_t)data_out;
   strides[n_surv] = (uint64_t)D.B * S;
-  std::string err;
-  if (K->pace) c->traced = K;
-  rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err, c->max_ctas);
-  if (rc) return fail(rc, err);
-  return PMRC_OK;
+  return run_plan(c, key, *spec, ptrs.data(), strides.data(), S, stripes, stream);
 }
 
 int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *in, size_t in_stride, void *out,
@@ -881,34 +1070,27 @@ int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *i
   char kb[96];
   snprintf(kb, sizeof kb, "apply:%dx%d:%016llx", rows, cols, (unsigned long long)h);
   const std::string key = kb;
-  Kernel *K = nullptr;
-  auto it = c->plans.find(key);
-  if (c->dry || it == c->plans.end()) {
-    PlanSpec spec;
-    spec.n_slots = 2;
-    for (int x = 0; x < cols; x++) spec.inputs.push_back({{{0, x, 1}}});
-    for (int r = 0; r < rows; r++) spec.outputs.push_back({1, r});
-    spec.A = Mat(rows, cols);
-    memcpy(spec.A.a.data(), A, (size_t)rows * cols);
-    bool any = false;
-    for (uint8_t v : spec.A.a) any |= v != 0;
-    if (!any) return fail(PMRC_EINVAL, "all-zero matrix (nothing to compute)");
-    int rc = get_kernel(c, key, spec, &K);
-    if (rc) return rc;
-  } else {
-    K = it->second.get();
+  bool any = false;
+  for (long i = 0; i < (long)rows * cols; i++) any |= A[i] != 0;
+  if (!any) return fail(PMRC_EINVAL, "all-zero matrix (nothing to compute)");
+  const PlanSpec *spec = nullptr;
+  int rc = get_spec(c, key, [&](PlanSpec &sp) {
+    sp.n_slots = 2;
+    for (int x = 0; x < cols; x++) sp.inputs.push_back({{{0, x, 1}}});
+    for (int r = 0; r < rows; r++) sp.outputs.push_back({1, r});
+    sp.A = Mat(rows, cols);
+    memcpy(sp.A.a.data(), A, (size_t)rows * cols);
+    return PMRC_OK;
+  }, &spec);
+  if (rc) return rc;
+  if (!c->dry && stripes && S) {
+    rc = check_region(in, in_stride, stripes);
+    if (!rc) rc = check_region(out, out_stride, stripes);
+    if (rc) return fail(rc, "bad in/out region");
   }
-  if (!stripes || !S) return PMRC_OK;
-  int rc = check_region(in, in_stride, stripes);
-  if (!rc) rc = check_region(out, out_stride, stripes);
-  if (rc) return fail(rc, "bad in/out region");
   uint64_t ptrs[2] = {(uint64_t)(uintptr_t)in, (uint64_t)(uintptr_t)out};
   uint64_t strides[2] = {(uint64_t)in_stride, (uint64_t)out_stride};
-  std::string err;
-  if (K->pace) c->traced = K;
-  rc = launch_kernel(*K, ptrs, strides, S, stripes, stream, err, c->max_ctas);
-  if (rc) return fail(rc, err);
-  return PMRC_OK;
+  return run_plan(c, key, *spec, ptrs, strides, S, stripes, stream);
 }
 
 int pmrc_set_max_ctas(pmrc_code *c, int max_ctas) {
@@ -917,11 +1099,19 @@ int pmrc_set_max_ctas(pmrc_code *c, int max_ctas) {
   return PMRC_OK;
 }
 
+int pmrc_set_plan_policy(pmrc_code *c, int policy) {
+  if (!c || policy < PMRC_PLAN_AUTO || policy > PMRC_PLAN_RUNTIME) return fail(PMRC_EINVAL, "bad argument");
+  c->policy = policy;
+  return PMRC_OK;
+}
+
+int pmrc_get_plan_policy(const pmrc_code *c) { return c ? c->policy : PMRC_EINVAL; }
+
 int pmrc_set_independent_launches(pmrc_code *c, int on) {
   if (!c || on < 0 || on > 1) return fail(PMRC_EINVAL, "bad argument");
   const int want = on ? 2 : 0;
   if (c->gen.pdl == want) return PMRC_OK;
-  // the kernels are generated with or without griddepcontrol.wait: drop the built ones (they are
+  // the kernels are generated with or without the PDL prologue: drop the built ones (they are
   // rebuilt on next use, from the in-tree cubin cache when present) after the device is idle
   if ((c->enc_built || !c->plans.empty()) && cudaDeviceSynchronize() != cudaSuccess) {
     cudaGetLastError();
@@ -933,7 +1123,6 @@ int pmrc_set_independent_launches(pmrc_code *c, int on) {
   c->enc_built = false;
   for (auto &kv : c->plans) free_kernel(*kv.second);
   c->plans.clear();
-  c->plan_meta.clear();
   c->traced = nullptr;
   return PMRC_OK;
 }
@@ -965,117 +1154,35 @@ int pmrc_repair(pmrc_code *c, int lost_id, const int *helper_ids_in, int n_helpe
   int need = 0;
   int rc = repair_common(c, lost_id, helper_ids_in, n_helpers, &need);
   if (rc) return rc;
-  // canonical helper order (the plan depends on the helper SET; the repaired piece is unique)
-  std::vector<int> help_v;
-  std::vector<pmrc_cregion> hp_v;
-  canonical_order(helper_ids_in, helper_pieces_in, n_helpers, help_v, hp_v);
-  const int *helper_ids = help_v.data();
-  const pmrc_cregion *helper_pieces = hp_v.data();
   if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
-  const CodeDef &D = c->def;
-  const std::string key = ids_key("rep", helper_ids, n_helpers, lost_id);
-  auto fe = c->plan_err.find(key);
-  if (fe != c->plan_err.end()) return fail(fe->second, "helper matrix singular (cached)");
-  Kernel *K = nullptr;
-  if (c->w == 16 && (c->dry || !c->plans.count(key))) {
-    // GF(2^16) (w = 16): mu = phi_f (P:53 footnote), R = [I_alpha | lambda_f I_alpha] Psi_H^{-1}
-    const GF65536 &F = gf16();
-    const int dd = D.d, a = D.alpha;
-    std::vector<uint16_t> Wm((size_t)dd * dd), Inv((size_t)dd * dd, 0);
-    for (int r = 0; r < dd; r++) {
-      for (int x = 0; x < dd; x++) Wm[(size_t)r * dd + x] = c->psi16[(size_t)helper_ids[r] * dd + x];
-      Inv[(size_t)r * dd + r] = 1;
-    }
-    for (int col = 0; col < dd; col++) {
-      int piv = -1;
-      for (int r = col; r < dd; r++)
-        if (Wm[(size_t)r * dd + col]) { piv = r; break; }
-      if (piv < 0) {
-        c->plan_err[key] = PMRC_ESINGULAR;
-        return fail(PMRC_ESINGULAR, "Psi_H singular for this (lost, helpers) pair (DESIGN.md R10)");
-      }
-      if (piv != col)
-        for (int x = 0; x < dd; x++) {
-          std::swap(Wm[(size_t)piv * dd + x], Wm[(size_t)col * dd + x]);
-          std::swap(Inv[(size_t)piv * dd + x], Inv[(size_t)col * dd + x]);
-        }
-      const uint16_t sc = F.inv(Wm[(size_t)col * dd + col]);
-      for (int x = 0; x < dd; x++) {
-        Wm[(size_t)col * dd + x] = F.mul(Wm[(size_t)col * dd + x], sc);
-        Inv[(size_t)col * dd + x] = F.mul(Inv[(size_t)col * dd + x], sc);
-      }
-      for (int r = 0; r < dd; r++) {
-        const uint16_t f = r == col ? 0 : Wm[(size_t)r * dd + col];
-        if (!f) continue;
-        for (int x = 0; x < dd; x++) {
-          Wm[(size_t)r * dd + x] ^= F.mul(f, Wm[(size_t)col * dd + x]);
-          Inv[(size_t)r * dd + x] ^= F.mul(f, Inv[(size_t)col * dd + x]);
-        }
-      }
-    }
-    const uint16_t lf = c->lam16[lost_id];
-    PlanSpec spec;
-    spec.w = 16;
-    spec.n_slots = n_helpers + 1;
-    for (int h = 0; h < n_helpers; h++) {
-      InputDesc in;
-      for (int b = 0; b < a; b++) {
-        const uint16_t mu = c->psi16[(size_t)lost_id * dd + b];
-        if (mu) in.terms.push_back({h, b, mu});
-      }
-      spec.inputs.push_back(in);
-    }
-    for (int q = 0; q < a; q++) spec.outputs.push_back({n_helpers, q});
-    spec.A = Mat(a, n_helpers);
-    spec.A16.assign((size_t)a * n_helpers, 0);
-    for (int q = 0; q < a; q++)
-      for (int h = 0; h < n_helpers; h++) {
-        const uint16_t v = Inv[(size_t)q * dd + h] ^ F.mul(lf, Inv[(size_t)(a + q) * dd + h]);
-        spec.A16[(size_t)q * n_helpers + h] = v;
-        spec.A.at(q, h) = v ? 1 : 0;
-      }
-    rc = get_kernel(c, key, spec, &K);
-    if (rc) return rc;
-  } else if (c->dry || !c->plans.count(key)) {
-    Mat R;
-    if (!repair_matrix(D, lost_id, helper_ids, R)) {
-      c->plan_err[key] = PMRC_ESINGULAR;
-      return fail(PMRC_ESINGULAR, "Psi_H singular for this (lost, helpers) pair (DESIGN.md R10)");
-    }
-    // fused plan: input h = beta_h = mu . piece_h (derived), outputs = alpha blocks
-    std::vector<uint8_t> mu = repair_mu(D, lost_id);
-    PlanSpec spec;
-    spec.n_slots = n_helpers + 1;
-    for (int h = 0; h < n_helpers; h++) {
-      InputDesc in;
-      for (size_t b = 0; b < mu.size(); b++)
-        if (mu[b]) in.terms.push_back({h, (int)b, mu[b]});
-      spec.inputs.push_back(in);
-    }
-    for (int a = 0; a < D.alpha; a++) spec.outputs.push_back({n_helpers, a});
-    spec.A = R;
-    rc = get_kernel(c, key, spec, &K);
-    if (rc) return rc;
-  } else {
-    K = c->plans[key].get();
-  }
-  if (!stripes || !S) return PMRC_OK;
+  // canonical helper order (the plan depends on the helper SET; the repaired piece is unique)
+  std::vector<int> H;
+  std::vector<pmrc_cregion> hp;
+  canonical_order(helper_ids_in, helper_pieces_in, n_helpers, H, hp);
+  const std::string key = ids_key("rep", H.data(), n_helpers, lost_id);
+  std::vector<int> slot_of(n_helpers);
+  for (int q = 0; q < n_helpers; q++) slot_of[q] = q;
+  const PlanSpec *spec = nullptr;
+  rc = get_spec(c, key, [&](PlanSpec &sp) {
+    return repair_spec(c, lost_id, H.data(), n_helpers, slot_of.data(), n_helpers, n_helpers + 1, sp);
+  }, &spec);
+  if (rc) return rc;
   std::vector<uint64_t> ptrs(n_helpers + 1), strides(n_helpers + 1);
-  for (int h = 0; h < n_helpers; h++) {
-    rc = check_region(helper_pieces[h].ptr, helper_pieces[h].stripe_stride, stripes);
-    if (rc) return fail(rc, "bad helper piece region");
-    ptrs[h] = (uint64_t)(uintptr_t)helper_pieces[h].ptr;
-    strides[h] = helper_pieces[h].stripe_stride;
+  if (!c->dry && stripes && S) {
+    for (int h = 0; h < n_helpers; h++) {
+      rc = check_region(hp[h].ptr, hp[h].stripe_stride, stripes);
+      if (rc) return fail(rc, "bad helper piece region");
+    }
+    rc = check_region(out_piece.ptr, out_piece.stripe_stride, stripes);
+    if (rc) return fail(rc, "bad output piece region");
   }
-  rc = check_region(out_piece.ptr, out_piece.stripe_stride, stripes);
-  if (rc) return fail(rc, "bad output piece region");
+  for (int h = 0; h < n_helpers; h++) {
+    ptrs[h] = (uint64_t)(uintptr_t)hp[h].ptr;
+    strides[h] = hp[h].stripe_stride;
+  }
   ptrs[n_helpers] = (uint64_t)(uintptr_t)out_piece.ptr;
   strides[n_helpers] = out_piece.stripe_stride;
-  std::string err;
-  if (K->pace) c->traced = K;
-  rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err, c->max_ctas);
-  if (rc) return fail(rc, err);
-  return PMRC_OK;
+  return run_plan(c, key, *spec, ptrs.data(), strides.data(), S, stripes, stream);
 }
 
 int pmrc_repair_project(pmrc_code *c, int lost_id, pmrc_cregion piece, pmrc_region beta, size_t S, size_t stripes,
@@ -1086,36 +1193,30 @@ int pmrc_repair_project(pmrc_code *c, int lost_id, pmrc_cregion piece, pmrc_regi
   if (lost_id < 0 || lost_id >= D.n) return fail(PMRC_EINVAL, "bad lost id");
   if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
   const std::string key = "proj:" + std::to_string(lost_id);
-  Kernel *K = nullptr;
-  if (!c->plans.count(key)) {
+  const PlanSpec *spec = nullptr;
+  int rc = get_spec(c, key, [&](PlanSpec &sp) {
     std::vector<uint8_t> mu = repair_mu(D, lost_id);
-    PlanSpec spec;
-    spec.n_slots = 2;
+    sp.n_slots = 2;
     std::vector<int> cols;
     for (size_t b = 0; b < mu.size(); b++)
       if (mu[b]) {
-        spec.inputs.push_back({{{0, (int)b, 1}}});  // only blocks with nonzero mu are read
+        sp.inputs.push_back({{{0, (int)b, 1}}});  // only blocks with nonzero mu are read
         cols.push_back((int)b);
       }
-    spec.outputs.push_back({1, 0});
-    spec.A = Mat(1, (int)cols.size());
-    for (size_t x = 0; x < cols.size(); x++) spec.A.at(0, (int)x) = mu[cols[x]];
-    int rc = get_kernel(c, key, spec, &K);
-    if (rc) return rc;
-  } else {
-    K = c->plans[key].get();
+    sp.outputs.push_back({1, 0});
+    sp.A = Mat(1, (int)cols.size());
+    for (size_t x = 0; x < cols.size(); x++) sp.A.at(0, (int)x) = mu[cols[x]];
+    return PMRC_OK;
+  }, &spec);
+  if (rc) return rc;
+  if (!c->dry && stripes && S) {
+    rc = check_region(piece.ptr, piece.stripe_stride, stripes);
+    if (!rc) rc = check_region(beta.ptr, beta.stripe_stride, stripes);
+    if (rc) return fail(rc, "bad piece/beta region");
   }
-  if (!stripes || !S) return PMRC_OK;
-  int rc = check_region(piece.ptr, piece.stripe_stride, stripes);
-  if (!rc) rc = check_region(beta.ptr, beta.stripe_stride, stripes);
-  if (rc) return fail(rc, "bad piece/beta region");
   uint64_t ptrs[2] = {(uint64_t)(uintptr_t)piece.ptr, (uint64_t)(uintptr_t)beta.ptr};
   uint64_t strides[2] = {piece.stripe_stride, beta.stripe_stride};
-  std::string err;
-  if (K->pace) c->traced = K;
-  rc = launch_kernel(*K, ptrs, strides, S, stripes, stream, err, c->max_ctas);
-  if (rc) return fail(rc, err);
-  return PMRC_OK;
+  return run_plan(c, key, *spec, ptrs, strides, S, stripes, stream);
 }
 
 int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids_in, int n_helpers,
@@ -1125,50 +1226,189 @@ int pmrc_repair_combine(pmrc_code *c, int lost_id, const int *helper_ids_in, int
   int need = 0;
   int rc = repair_common(c, lost_id, helper_ids_in, n_helpers, &need);
   if (rc) return rc;
-  std::vector<int> help_v;
-  std::vector<pmrc_cregion> b_v;
-  canonical_order(helper_ids_in, betas_in, n_helpers, help_v, b_v);
-  const int *helper_ids = help_v.data();
-  const pmrc_cregion *betas = b_v.data();
   if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
+  std::vector<int> H;
+  std::vector<pmrc_cregion> betas;
+  canonical_order(helper_ids_in, betas_in, n_helpers, H, betas);
   const CodeDef &D = c->def;
-  const std::string key = ids_key("comb", helper_ids, n_helpers, lost_id);
-  auto fe = c->plan_err.find(key);
-  if (fe != c->plan_err.end()) return fail(fe->second, "helper matrix singular (cached)");
-  Kernel *K = nullptr;
-  if (c->dry || !c->plans.count(key)) {
+  const std::string key = ids_key("comb", H.data(), n_helpers, lost_id);
+  const PlanSpec *spec = nullptr;
+  rc = get_spec(c, key, [&](PlanSpec &sp) {
     Mat R;
-    if (!repair_matrix(D, lost_id, helper_ids, R)) {
-      c->plan_err[key] = PMRC_ESINGULAR;
-      return fail(PMRC_ESINGULAR, "Psi_H singular for this (lost, helpers) pair (DESIGN.md R10)");
-    }
-    PlanSpec spec;
-    spec.n_slots = n_helpers + 1;
-    for (int h = 0; h < n_helpers; h++) spec.inputs.push_back({{{h, 0, 1}}});
-    for (int a = 0; a < D.alpha; a++) spec.outputs.push_back({n_helpers, a});
-    spec.A = R;
-    rc = get_kernel(c, key, spec, &K);
-    if (rc) return rc;
-  } else {
-    K = c->plans[key].get();
-  }
-  if (!stripes || !S) return PMRC_OK;
+    if (!repair_matrix(D, lost_id, H.data(), R)) return PMRC_ESINGULAR;
+    sp.n_slots = n_helpers + 1;
+    for (int h = 0; h < n_helpers; h++) sp.inputs.push_back({{{h, 0, 1}}});
+    for (int a = 0; a < D.alpha; a++) sp.outputs.push_back({n_helpers, a});
+    sp.A = R;
+    return PMRC_OK;
+  }, &spec);
+  if (rc) return rc;
   std::vector<uint64_t> ptrs(n_helpers + 1), strides(n_helpers + 1);
+  if (!c->dry && stripes && S) {
+    for (int h = 0; h < n_helpers; h++) {
+      rc = check_region(betas[h].ptr, betas[h].stripe_stride, stripes);
+      if (rc) return fail(rc, "bad beta region");
+    }
+    rc = check_region(out_piece.ptr, out_piece.stripe_stride, stripes);
+    if (rc) return fail(rc, "bad output piece region");
+  }
   for (int h = 0; h < n_helpers; h++) {
-    rc = check_region(betas[h].ptr, betas[h].stripe_stride, stripes);
-    if (rc) return fail(rc, "bad beta region");
     ptrs[h] = (uint64_t)(uintptr_t)betas[h].ptr;
     strides[h] = betas[h].stripe_stride;
   }
-  rc = check_region(out_piece.ptr, out_piece.stripe_stride, stripes);
-  if (rc) return fail(rc, "bad output piece region");
   ptrs[n_helpers] = (uint64_t)(uintptr_t)out_piece.ptr;
   strides[n_helpers] = out_piece.stripe_stride;
+  return run_plan(c, key, *spec, ptrs.data(), strides.data(), S, stripes, stream);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Batch calls: per-stripe failure patterns in ONE launch of the runtime-coefficient kernel
+// (config 4 as BASELINE.json states it).  Slots 0..n-1 are the nodes' piece regions, slot n the
+// output region; stripe t runs the plan of its own pattern.
+// ---------------------------------------------------------------------------------------------
+static int check_node_regions(const pmrc_code *c, const pmrc_cregion *nodes, const std::vector<char> &used,
+                              size_t stripes) {
+  for (int i = 0; i < c->def.n; i++) {
+    if (!used[i]) continue;
+    const int rc = check_region(nodes[i].ptr, nodes[i].stripe_stride, stripes);
+    if (rc) return fail(rc, "bad node piece region " + std::to_string(i));
+  }
+  return PMRC_OK;
+}
+
+// shared tail of the batch calls: per-stripe keys -> specs -> runtime plans of one shape -> launch
+static int run_batch(pmrc_code *c, const std::vector<std::string> &keys, const std::vector<const PlanSpec *> &specs,
+                     const pmrc_cregion *nodes, uint64_t out_ptr, uint64_t out_stride, size_t S, size_t stripes,
+                     void *stream) {
+  const int n = c->def.n;
+  int max_out = 0;
+  for (const PlanSpec *sp : specs)
+    if (sp) max_out = std::max(max_out, (int)sp->outputs.size());
+  if (!max_out || !S) return PMRC_OK;  // nothing to compute in any stripe
+  const pmrc_rt::RlcShape sh = rt_shape(max_out, c->gen);
+  std::vector<RtPlan *> plans;
+  std::map<std::string, uint16_t> idx;
+  std::vector<uint16_t> stripe_plan(stripes);
+  for (size_t t = 0; t < stripes; t++) {
+    if (!specs[t]) {
+      stripe_plan[t] = 0xFFFF;  // nothing to compute in this stripe
+      continue;
+    }
+    auto it = idx.find(keys[t]);
+    if (it == idx.end()) {
+      if (plans.size() >= 0xFFFF) return fail(PMRC_EUNSUPPORTED, "too many distinct patterns in one batch");
+      RtPlan *P = nullptr;
+      int rc = get_rt_plan(c, keys[t], *specs[t], sh.R, &P);
+      if (rc) return rc;
+      it = idx.insert({keys[t], (uint16_t)plans.size()}).first;
+      plans.push_back(P);
+    }
+    stripe_plan[t] = it->second;
+  }
+  std::vector<uint64_t> ptrs(n + 1), strides(n + 1);
+  for (int i = 0; i < n; i++) {
+    ptrs[i] = (uint64_t)(uintptr_t)nodes[i].ptr;
+    strides[i] = nodes[i].stripe_stride;
+  }
+  ptrs[n] = out_ptr;
+  strides[n] = out_stride;
+  int rc = ensure_device(c);
+  if (rc) return rc;
   std::string err;
-  if (K->pace) c->traced = K;
-  rc = launch_kernel(*K, ptrs.data(), strides.data(), S, stripes, stream, err, c->max_ctas);
+  rc = rt_launch(plans, stripe_plan.data(), ptrs.data(), strides.data(), n + 1, S, stripes, sh, stream, c->max_ctas,
+                 err);
   if (rc) return fail(rc, err);
   return PMRC_OK;
+}
+
+int pmrc_decode_batch(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregion *nodes, void *data_out,
+                      size_t S, size_t stripes, int *n_written, void *stream) {
+  if (!c || !surv_ids || !nodes || !data_out) return fail(PMRC_EINVAL, "NULL argument");
+  if (c->w != 8) return fail(PMRC_EUNSUPPORTED, "batch calls: GF(2^8) codes only");
+  const CodeDef &D = c->def;
+  if (n_surv < 1 || n_surv > D.n) return fail(PMRC_EINVAL, "bad survivor count");
+  if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
+  if (D.n + 1 > pmrc_rt::kRlcMaxSlots) return fail(PMRC_EUNSUPPORTED, "too many nodes for a batch launch");
+  std::vector<std::string> keys(stripes);
+  std::vector<const PlanSpec *> specs(stripes);
+  std::vector<char> used(D.n, 0);
+  std::vector<int> slot_of(D.n);
+  for (int i = 0; i < D.n; i++) slot_of[i] = i;
+  for (size_t t = 0; t < stripes; t++) {
+    const int *ids = surv_ids + t * (size_t)n_surv;
+    if (check_ids(D, ids, n_surv)) return fail(PMRC_EINVAL, "bad survivor ids in stripe " + std::to_string(t));
+    std::vector<int> s(ids, ids + n_surv);
+    std::sort(s.begin(), s.end());
+    keys[t] = ids_key("decn", s.data(), n_surv, 0);
+    std::vector<int> so(n_surv);
+    for (int q = 0; q < n_surv; q++) so[q] = s[q];  // slot = node id
+    int rc = get_spec(c, keys[t], [&](PlanSpec &sp) { return decode_spec(c, s.data(), n_surv, so.data(), D.n, D.n + 1,
+                                                                          sp); },
+                      &specs[t]);
+    if (rc) return fail(rc, std::string(pmrc_last_error()) + " (stripe " + std::to_string(t) + ")");
+    if (n_written) n_written[t] = c->plan_meta[keys[t]];
+    if (specs[t])
+      for (const auto &in : specs[t]->inputs)
+        for (const auto &tm : in.terms) used[tm.slot] = 1;
+  }
+  int rc = check_node_regions(c, nodes, used, stripes);
+  if (!rc) rc = check_region(data_out, (size_t)D.B * S, stripes);
+  if (rc) return fail(rc, "bad region");
+  return run_batch(c, keys, specs, nodes, (uint64_t)(uintptr_t)data_out, (uint64_t)D.B * S, S, stripes, stream);
+}
+
+int pmrc_repair_batch(pmrc_code *c, const int *lost_ids, const int *helper_ids, int n_helpers, const pmrc_cregion *nodes,
+                      pmrc_region out_piece, size_t S, size_t stripes, void *stream) {
+  if (!c || !lost_ids || !helper_ids || !nodes) return fail(PMRC_EINVAL, "NULL argument");
+  if (c->w != 8) return fail(PMRC_EUNSUPPORTED, "batch calls: GF(2^8) codes only");
+  const CodeDef &D = c->def;
+  if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
+  if (D.n + 1 > pmrc_rt::kRlcMaxSlots) return fail(PMRC_EUNSUPPORTED, "too many nodes for a batch launch");
+  std::vector<std::string> keys(stripes);
+  std::vector<const PlanSpec *> specs(stripes);
+  std::vector<char> used(D.n, 0);
+  for (size_t t = 0; t < stripes; t++) {
+    const int f = lost_ids[t];
+    const int *ids = helper_ids + t * (size_t)n_helpers;
+    int need = 0;
+    int rc = repair_common(c, f, ids, n_helpers, &need);
+    if (rc) return fail(rc, std::string(pmrc_last_error()) + " (stripe " + std::to_string(t) + ")");
+    std::vector<int> H(ids, ids + n_helpers);
+    std::sort(H.begin(), H.end());
+    keys[t] = ids_key("repn", H.data(), n_helpers, f);
+    rc = get_spec(c, keys[t], [&](PlanSpec &sp) {
+      return repair_spec(c, f, H.data(), n_helpers, H.data(), D.n, D.n + 1, sp);  // slot = node id
+    }, &specs[t]);
+    if (rc) return fail(rc, std::string(pmrc_last_error()) + " (stripe " + std::to_string(t) + ")");
+    for (const auto &in : specs[t]->inputs)
+      for (const auto &tm : in.terms) used[tm.slot] = 1;
+  }
+  int rc = check_node_regions(c, nodes, used, stripes);
+  if (!rc) rc = check_region(out_piece.ptr, out_piece.stripe_stride, stripes);
+  if (rc) return fail(rc, "bad region");
+  return run_batch(c, keys, specs, nodes, (uint64_t)(uintptr_t)out_piece.ptr, out_piece.stripe_stride, S, stripes,
+                   stream);
+}
+
+int pmrc_plan_prepare(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids) {
+  // promote a (hot) failure pattern to its generated bitsliced kernel: build + NVRTC-compile (or
+  // load from the kernel cache) now, so later calls with this pattern run the JIT kernel under
+  // PMRC_PLAN_AUTO
+  if (!c || !ids) return fail(PMRC_EINVAL, "NULL argument");
+  const int saved = c->policy;
+  c->policy = PMRC_PLAN_JIT;
+  std::vector<pmrc_cregion> pieces(std::max(1, n_ids), pmrc_cregion{(const void *)(uintptr_t)4096, 0});
+  int rc;
+  if (op == 0) {
+    int nw = 0;
+    rc = pmrc_decode(c, ids, n_ids, pieces.data(), (void *)(uintptr_t)4096, 16, 0, &nw, nullptr);
+  } else if (op == 1) {
+    rc = pmrc_repair(c, lost_id, ids, n_ids, pieces.data(), pmrc_region{(void *)(uintptr_t)4096, 0}, 16, 0, nullptr);
+  } else {
+    rc = fail(PMRC_EINVAL, "op must be 0 (decode) or 1 (repair)");
+  }
+  c->policy = saved;
+  return rc;
 }
 
 }  // extern "C"

@@ -1,0 +1,280 @@
+// Host side of the runtime-coefficient kernel (see rtplan.hpp and csrc/rt/rlc.cu).
+#include "rtplan.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "../../../include/pmrc.h"
+#include "../rt/rlc.hpp"
+
+namespace pmrc {
+
+using pmrc_rt::RlcArgs;
+using pmrc_rt::RlcHdr;
+
+pmrc_rt::RlcShape rt_shape(int n_out, const GenOptions &o) {
+  // R rows x V words of accumulators per thread, G row groups of GT threads per CTA (a pass covers
+  // G R rows; measured, profiles/r02):
+  //   <= 8 rows (repair, projections, RS encode): (8, 4, 1, 256), two CTAs per SM
+  //   more (decode, encode): (8, 4, 2, 256), 16 rows per pass (shapes with V = 2 and more groups
+  //   measured slower: twice the per-word instruction overhead)
+  // (rt_groups overrides for experiments; tg is set per launch from the plans)
+  pmrc_rt::RlcShape sh = n_out <= 8 ? pmrc_rt::RlcShape{8, 4, 1, 256, false} : pmrc_rt::RlcShape{8, 4, 2, 256, false};
+  if (o.rt_groups == 1 || o.rt_groups == 2) sh.G = o.rt_groups;
+  return sh;
+}
+
+// PRMT tables of coefficient c (rlc.cu): T0[j] = c*j, T1[j] = c*(j<<3) (j < 8), T2[j] = c*(j<<6) (j < 4),
+// little-endian bytes: (T0a, T0b, T1a, T1b) and T2
+static void tables(uint8_t c, uint32_t *a4, uint32_t *b1) {
+  const GF256 &F = gf();
+  uint8_t t0[8], t1[8], t2[4];
+  for (int j = 0; j < 8; j++) {
+    t0[j] = F.mul(c, (uint8_t)j);
+    t1[j] = F.mul(c, (uint8_t)(j << 3));
+  }
+  for (int j = 0; j < 4; j++) t2[j] = F.mul(c, (uint8_t)(j << 6));
+  auto pk = [](const uint8_t *b) {
+    return (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+  };
+  a4[0] = pk(t0);
+  a4[1] = pk(t0 + 4);
+  a4[2] = pk(t1);
+  a4[3] = pk(t1 + 4);
+  *b1 = pk(t2);
+}
+
+int rt_build(const PlanSpec &p, int R, RtPlan &out, std::string &err) {
+  if (p.w != 8) {
+    err = "runtime-coefficient kernel: GF(2^8) plans only";
+    return PMRC_EUNSUPPORTED;
+  }
+  if (p.n_slots > pmrc_rt::kRlcMaxSlots) {
+    err = "runtime-coefficient kernel: too many slots";
+    return PMRC_EUNSUPPORTED;
+  }
+  const int n_in = (int)p.inputs.size(), n_out = (int)p.outputs.size();
+  int n_terms = 0;
+  for (const auto &in : p.inputs) n_terms += (int)in.terms.size();
+  if (n_in == 0 || n_out == 0 || n_in > 65535 || n_terms > 65535) {
+    err = "runtime-coefficient kernel: bad plan size";
+    return PMRC_EUNSUPPORTED;
+  }
+  const int n_rb = (n_out + R - 1) / R;  // row blocks of R rows (a pass runs G of them)
+  // layout (words): header 16 | tabA 4*n_in*n_out | ttabA 4*n_terms | tabB n_in*n_out | ttabB n_terms |
+  //                 terms 2*n_terms | outs 2*n_out | masks n_in*n_rb      (16-B aligned uint4 arrays first)
+  RlcHdr h = {};
+  h.magic = pmrc_rt::kRlcMagic;
+  h.n_in = n_in;
+  h.n_out = n_out;
+  h.n_terms = n_terms;
+  h.R = R;
+  h.n_rb = n_rb;
+  uint32_t w = 16;
+  h.off_ttabA = w;
+  w += 4u * n_terms;
+  h.off_ttabB = w;
+  w += n_terms;
+  h.off_terms = w;
+  w += 2u * n_terms;
+  h.off_outs = w;
+  w += 2u * n_out;
+  h.off_masks = w;
+  w += (uint32_t)n_in * n_rb;
+  w = (w + 3u) & ~3u;  // tabA is read as uint4
+  h.off_tabA = w;
+  w += 4u * n_in * n_out;
+  h.off_tabB = w;
+  w += (uint32_t)n_in * n_out;
+  h.words = w;
+  h.smem_words = w;
+  if (w > (uint32_t)pmrc_rt::kRlcMaxPlanWords) {
+    // tables too large for shared memory: the kernel reads them from the blob in device memory
+    h.flags |= pmrc_rt::kRlcGlobalTables;
+    h.smem_words = h.off_tabA;
+    if (h.smem_words > (uint32_t)pmrc_rt::kRlcMaxPlanWords) {
+      err = "runtime-coefficient kernel: plan wiring too large (" + std::to_string(h.smem_words * 4) + " bytes)";
+      return PMRC_EUNSUPPORTED;
+    }
+  }
+  // row order: rows of equal support side by side, densest first (sparse MSR encode: the n-k rows
+  // of a PM symbol index share their support, so every R-row block is all or nothing per input);
+  // the kernel runs a block without per-row branches when every row of it reads the input
+  std::vector<int> ord(n_out);
+  for (int r = 0; r < n_out; r++) ord[r] = r;
+  {
+    std::vector<std::vector<uint8_t>> sup(n_out, std::vector<uint8_t>(n_in));
+    std::vector<int> cnt(n_out, 0);
+    for (int r = 0; r < n_out; r++)
+      for (int i = 0; i < n_in; i++) cnt[r] += (sup[r][i] = p.A.at(r, i) != 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+      if (cnt[x] != cnt[y]) return cnt[x] > cnt[y];
+      return sup[x] > sup[y];
+    });
+  }
+  std::vector<uint32_t> b(w, 0u);
+  long nnz = 0;
+  for (int i = 0; i < n_in; i++)
+    for (int r = 0; r < n_out; r++) {
+      const uint8_t c = p.A.at(ord[r], i);
+      if (!c) continue;
+      nnz++;
+      const size_t e = (size_t)i * n_out + r;
+      tables(c, &b[h.off_tabA + 4 * e], &b[h.off_tabB + e]);
+      b[h.off_masks + (size_t)i * n_rb + r / R] |= 1u << (r % R);
+    }
+  int q = 0;
+  for (int i = 0; i < n_in; i++) {
+    const auto &terms = p.inputs[i].terms;
+    for (size_t j = 0; j < terms.size(); j++, q++) {
+      const Term &t = terms[j];
+      if (t.slot < 0 || t.slot >= p.n_slots || t.blk < 0 || t.blk > 65535 || t.coef == 0 || t.coef > 255) {
+        err = "runtime-coefficient kernel: bad term";
+        return PMRC_EUNSUPPORTED;
+      }
+      uint32_t w0 = (uint32_t)t.slot;
+      if (j + 1 == terms.size()) w0 |= 0x40000000u;
+      if (t.coef == 1) w0 |= 0x80000000u;
+      else tables((uint8_t)t.coef, &b[h.off_ttabA + 4 * q], &b[h.off_ttabB + q]);
+      b[h.off_terms + 2 * q] = w0;
+      b[h.off_terms + 2 * q + 1] = (uint32_t)t.blk | ((uint32_t)i << 16);
+    }
+  }
+  for (int r = 0; r < n_out; r++) {
+    const OutputDesc &o = p.outputs[ord[r]];
+    if (o.slot < 0 || o.slot >= p.n_slots || o.blk < 0) {
+      err = "runtime-coefficient kernel: bad output";
+      return PMRC_EUNSUPPORTED;
+    }
+    b[h.off_outs + 2 * r] = (uint32_t)o.slot;
+    b[h.off_outs + 2 * r + 1] = (uint32_t)o.blk;
+  }
+  memcpy(b.data(), &h, sizeof h);
+  rt_free(out);
+  out.blob = std::move(b);
+  out.R = R;
+  out.n_in = n_in;
+  out.n_out = n_out;
+  out.n_terms = n_terms;
+  out.nnz = nnz;
+  return PMRC_OK;
+}
+
+void rt_free(RtPlan &p) {
+  if (p.dev) cudaFree(p.dev);
+  p.dev = nullptr;
+}
+
+static int sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 148;
+  }
+  return n;
+}
+
+int rt_launch(const std::vector<RtPlan *> &plans, const uint16_t *stripe_plan, const uint64_t *ptrs,
+              const uint64_t *strides, int n_slots, size_t S, size_t stripes, const pmrc_rt::RlcShape &sh,
+              void *stream, int max_ctas, std::string &err) {
+  if (S == 0 || stripes == 0) return PMRC_OK;
+  if (plans.empty() || n_slots > pmrc_rt::kRlcMaxSlots) {
+    err = "rt_launch: bad arguments";
+    return PMRC_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned max_words = 0;
+  bool tg = false;
+  for (RtPlan *p : plans) {
+    tg |= (p->blob[7] & pmrc_rt::kRlcGlobalTables) != 0;
+    if (p->R != sh.R) {
+      err = "rt_launch: plans of one launch must share their shape";
+      return PMRC_EINVAL;
+    }
+    max_words = std::max(max_words, p->blob[15]);  // smem_words
+    if (!p->dev) {
+      const size_t nb = p->blob.size() * 4;
+      if (cudaMalloc(&p->dev, nb) != cudaSuccess) {
+        cudaGetLastError();
+        p->dev = nullptr;
+        err = "cudaMalloc(plan)";
+        return PMRC_ENOMEM;
+      }
+      // the host blob lives in the cached plan, so the async copy's source outlives it
+      if (cudaMemcpyAsync(p->dev, p->blob.data(), nb, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+        err = std::string("plan upload: ") + cudaGetErrorString(cudaGetLastError());
+        return PMRC_ECUDA;
+      }
+    }
+  }
+  RlcArgs a;
+  memset(&a, 0, sizeof a);
+  a.S = S;
+  a.stripes = stripes;
+  a.max_words = max_words;
+  a.n_slots = (unsigned)n_slots;
+  a.sh3 = 1u << 29;
+  a.sh6 = 1u << 26;
+  a.sh12 = 1u << 20;
+  for (int i = 0; i < n_slots; i++) {
+    a.slot_ptr[i] = ptrs[i];
+    a.slot_stride[i] = strides[i];
+  }
+  void *scratch = nullptr;
+  if (stripe_plan) {
+    // per-call launch tables (plan addresses + the stripes' plan indices) in stream-ordered memory
+    const size_t np = plans.size(), bytes = np * 8 + stripes * 2;
+    std::vector<uint8_t> host(bytes);
+    for (size_t i = 0; i < np; i++) {
+      const uint64_t d = (uint64_t)(uintptr_t)plans[i]->dev;
+      memcpy(host.data() + 8 * i, &d, 8);
+    }
+    for (size_t t = 0; t < stripes; t++) {
+      if (stripe_plan[t] >= np && stripe_plan[t] != 0xFFFF) {  // 0xFFFF: nothing to compute in stripe t
+        err = "rt_launch: stripe plan index out of range";
+        return PMRC_EINVAL;
+      }
+    }
+    memcpy(host.data() + 8 * np, stripe_plan, stripes * 2);
+    if (cudaMallocAsync(&scratch, bytes, st) != cudaSuccess) {
+      cudaGetLastError();
+      err = "cudaMallocAsync(launch tables)";
+      return PMRC_ENOMEM;
+    }
+    // pageable source: staged before cudaMemcpyAsync returns, so `host` may go out of scope
+    if (cudaMemcpyAsync(scratch, host.data(), bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+      err = std::string("launch tables: ") + cudaGetErrorString(cudaGetLastError());
+      return PMRC_ECUDA;
+    }
+    a.plan_ptrs = (const unsigned long long *)scratch;
+    a.stripe_plan = (const uint16_t *)((uint8_t *)scratch + 8 * np);
+  } else {
+    a.plan0 = (const uint32_t *)plans[0]->dev;
+  }
+  const uint64_t TP = (uint64_t)sh.GT * sh.V * 4;
+  const uint64_t items = (S + TP - 1) / TP * (uint64_t)stripes;
+  pmrc_rt::RlcShape shx = sh;
+  shx.tg = tg;
+  int per_sm = pmrc_rt::rlc_ctas_per_sm(shx, max_words);
+  if (per_sm < 1) {
+    err = "runtime-coefficient kernel does not fit on an SM (plan too large)";
+    if (scratch) cudaFreeAsync(scratch, st);
+    return PMRC_EUNSUPPORTED;
+  }
+  uint64_t grid = (uint64_t)sm_count() * per_sm;
+  if (max_ctas > 0) grid = std::min<uint64_t>(grid, (uint64_t)max_ctas);
+  grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, items));
+  const int rc = pmrc_rt::rlc_launch(a, shx, (int)grid, stream);
+  if (scratch) cudaFreeAsync(scratch, st);
+  if (rc) {
+    err = rc == -2 ? "runtime-coefficient kernel: no instantiation for this shape"
+                   : std::string("runtime-coefficient launch: ") + cudaGetErrorString(cudaGetLastError());
+    return rc == -2 ? PMRC_EUNSUPPORTED : PMRC_ECUDA;
+  }
+  launch_counter()++;
+  return PMRC_OK;
+}
+
+}  // namespace pmrc

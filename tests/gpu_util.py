@@ -1,6 +1,7 @@
 """Helpers for the GPU parity tests: device buffers (torch, plumbing only), node piece views and
 oracle comparisons.  Inputs come from the shared seeded generator (inputs/)."""
 import numpy as np
+import pytest
 import torch
 
 import inputs
@@ -13,10 +14,12 @@ DEV = torch.device("cuda:0")
 class Stripes:
     """Data of `stripes` stripes on the device + its parity through the C ABI."""
 
-    def __init__(self, kind, k, n, S, stripes, seed, device_fill=False):
+    def __init__(self, kind, k, n, S, stripes, seed, device_fill=False, policy=None):
         self.kind, self.k, self.n, self.S, self.stripes = kind, k, n, S, stripes
         self.d = k if kind == pm.PMRC_RS_VANDERMONDE else 2 * k - 2
         self.code = pm.pmrc_create(kind, k, self.d, n)
+        if policy is not None:
+            pm.pmrc_set_plan_policy(self.code, policy)
         info = pm.pmrc_info(self.code)
         self.alpha, self.B, self.P = info["alpha"], info["B"], info["parity_rows"]
         self.seed = seed
@@ -63,6 +66,15 @@ class Stripes:
             return self.data[:, i * a:(i + 1) * a]
         self.piece(i)
         return self._mbr_sys[i]
+
+
+    def nodes(self):
+        """(ptr, stripe_stride) of every node's piece (the batch calls' node table)."""
+        return [self.piece(i) for i in range(self.n)]
+
+
+# both engines of every decode / repair / apply test (include/pmrc.h: results are bit-identical)
+POLICIES = [pytest.param(pm.PMRC_PLAN_JIT, id="jit"), pytest.param(pm.PMRC_PLAN_RUNTIME, id="runtime")]
 
 
 def oracle_kind(kind):

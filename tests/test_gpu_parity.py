@@ -10,7 +10,7 @@ import torch
 import inputs
 import oracle as O
 import paper_1412_3022_b200 as pm
-from gpu_util import DEV, Stripes, oracle_kind
+from gpu_util import DEV, POLICIES, Stripes, oracle_kind
 
 pytestmark = pytest.mark.gpu
 
@@ -34,9 +34,10 @@ ENC_CASES = [
 ]
 
 
+@pytest.mark.parametrize("policy", POLICIES)
 @pytest.mark.parametrize("kind,k,n,S,stripes", ENC_CASES)
-def test_encode_bit_exact(kind, k, n, S, stripes):
-    st = Stripes(kind, k, n, S, stripes, seed=11 + k)
+def test_encode_bit_exact(kind, k, n, S, stripes, policy):
+    st = Stripes(kind, k, n, S, stripes, seed=11 + k, policy=policy)
     try:
         st.encode()
         want = O.encode(oracle_kind(kind), n, k, st.d, st.host_data())
@@ -76,11 +77,12 @@ def test_encode_does_not_touch_beyond_parity():
         st.close()
 
 
+@pytest.mark.parametrize("policy", POLICIES)
 @pytest.mark.parametrize("kind", [pm.PMRC_MSR_SPARSE, pm.PMRC_MSR_VANILLA, pm.PMRC_MBR, pm.PMRC_RS_VANDERMONDE])
-def test_decode_config1_every_subset(kind):
+def test_decode_config1_every_subset(kind, policy):
     # config 1: k=3, n=6 (RS uses the same k, n): decode from every 3-subset
     k, n, S, stripes = 3, 6, 2048, 16
-    st = Stripes(kind, k, n, S, stripes, seed=1)
+    st = Stripes(kind, k, n, S, stripes, seed=1, policy=policy)
     try:
         st.encode()
         # the parity every decode starts from is itself the oracle's (not only self-consistent)
@@ -103,10 +105,11 @@ def test_decode_config1_every_subset(kind):
         st.close()
 
 
+@pytest.mark.parametrize("policy", POLICIES)
 @pytest.mark.parametrize("kind", [pm.PMRC_MSR_SPARSE, pm.PMRC_MBR])
-def test_decode_k8_random_subsets(kind):
+def test_decode_k8_random_subsets(kind, policy):
     k, n, S, stripes = 8, 16, 2048 + 16, 2
-    st = Stripes(kind, k, n, S, stripes, seed=9)
+    st = Stripes(kind, k, n, S, stripes, seed=9, policy=policy)
     try:
         st.encode()
         r = inputs.rng(4)
@@ -157,10 +160,11 @@ def _predicted_singular(kind, k, n, f, H):
     return f < alpha and len(omitted) == 1 and omitted[0] < alpha
 
 
+@pytest.mark.parametrize("policy", POLICIES)
 @pytest.mark.parametrize("kind", [pm.PMRC_MSR_SPARSE, pm.PMRC_MSR_VANILLA, pm.PMRC_MBR, pm.PMRC_MSR_SPARSE_N2K])
-def test_repair_config1_every_node_every_helper_set(kind):
+def test_repair_config1_every_node_every_helper_set(kind, policy):
     k, n, S, stripes = 3, 6, 2048, 16
-    st = Stripes(kind, k, n, S, stripes, seed=1)
+    st = Stripes(kind, k, n, S, stripes, seed=1, policy=policy)
     try:
         st.encode()
         assert np.array_equal(st.parity.cpu().numpy(), O.encode(oracle_kind(kind), n, k, st.d, st.host_data()))
@@ -185,10 +189,11 @@ def test_repair_config1_every_node_every_helper_set(kind):
         st.close()
 
 
+@pytest.mark.parametrize("policy", POLICIES)
 @pytest.mark.parametrize("kind", [pm.PMRC_MSR_SPARSE, pm.PMRC_MBR, pm.PMRC_RS_VANDERMONDE])
-def test_repair_k8_random(kind):
+def test_repair_k8_random(kind, policy):
     k, n, S, stripes = 8, 16, 4096 + 16, 2
-    st = Stripes(kind, k, n, S, stripes, seed=21)
+    st = Stripes(kind, k, n, S, stripes, seed=21, policy=policy)
     try:
         st.encode()
         r = inputs.rng(8)
@@ -209,10 +214,11 @@ def test_repair_k8_random(kind):
         st.close()
 
 
-def test_repair_project_combine_split_equals_oracle():
+@pytest.mark.parametrize("policy", POLICIES)
+def test_repair_project_combine_split_equals_oracle(policy):
     # helper side (projection) and newcomer side (combine) as separate calls, vs the oracle
     k, n, S, stripes = 8, 16, 2048, 2
-    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=33)
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=33, policy=policy)
     try:
         st.encode()
         for f in (2, 11):
@@ -296,13 +302,15 @@ def _full_job(kind, k, S, seed):
     return code, data, par, (n, d, B, P, a, stripes, real, stream)
 
 
-def test_full_size_config4_repair_and_decode():
+@pytest.mark.parametrize("policy", POLICIES)
+def test_full_size_config4_repair_and_decode(policy):
     # config 4 at full size (1 GiB, 1 MiB sub-blocks, 19 stripes) in the sweep's launch
     # configuration: a repair of a parity node (alpha blocks per helper) and of a systematic node
     # (1 block per helper) regenerate the encoded pieces exactly; decode from a random
     # 8-subset returns the data; a sampled window of the parity is checked against the oracle
     k, S = 8, 1 << 20
     code, data, par, (n, d, B, P, a, stripes, real, stream) = _full_job(pm.PMRC_MSR_SPARSE, k, S, 99)
+    pm.pmrc_set_plan_policy(code, policy)
     try:
         def piece(i):
             return (par.data_ptr() + (i - k) * a * S, P * S) if i >= k else (data.data_ptr() + i * a * S, B * S)
@@ -328,11 +336,13 @@ def test_full_size_config4_repair_and_decode():
         pm.pmrc_destroy(code)
 
 
-def test_full_size_config3_mbr_encode_decode():
+@pytest.mark.parametrize("policy", POLICIES)
+def test_full_size_config3_mbr_encode_decode(policy):
     # config 3 at full size (MBR k=8, 1 GiB, 256 KiB sub-blocks, 49 stripes): sampled parity windows
     # vs the oracle, then decode from a random 8-subset of nodes returns every missing data block
     k, S = 8, 256 << 10
     code, data, par, (n, d, B, P, a, stripes, real, stream) = _full_job(pm.PMRC_MBR, k, S, 7)
+    pm.pmrc_set_plan_policy(code, policy)
     try:
         for t, p0 in ((0, 0), (stripes - 2, S - 1024), (17, 77 * 16)):
             x = np.stack([inputs.host_bytes(1024, 7, t * B * S + c * S + p0, real) for c in range(B)])
@@ -411,13 +421,14 @@ def test_n2k_extension_repairs_paper_singular_sets_k8():
         ext.close()
 
 
-def test_apply_matches_encode_specific_and_precode_paths():
+@pytest.mark.parametrize("policy", POLICIES)
+def test_apply_matches_encode_specific_and_precode_paths(policy):
     # pmrc_apply (general region linear combination) on the paper's comparison paths:
     #  * non-systematic encode Y = G Z equals the oracle's specific PM encode C = Psi M(Z)
     #  * precode Z = Gtilde^{-1} X, then parity = G_parity Z, equals the linearised systematic
     #    encode G'' X (the two systematic encoders give identical codewords)
     k, n, S, stripes = 8, 16, 2048 + 48, 2
-    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=81)
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=81, policy=policy)
     try:
         st.encode()
         G = pm.pmrc_matrix(st.code, pm.MATRIX_G)
@@ -443,12 +454,13 @@ def test_apply_matches_encode_specific_and_precode_paths():
         st.close()
 
 
-def test_decode_and_repair_write_only_their_outputs():
+@pytest.mark.parametrize("policy", POLICIES)
+def test_decode_and_repair_write_only_their_outputs(policy):
     # no compute-sanitizer on this pool: bounds by sentinels instead.  Decode writes exactly the
     # missing data blocks (every other byte of data_out keeps its sentinel); repair writes exactly
     # stripes x alpha x S bytes (guard bytes after the piece stay intact); ragged S
     k, n, S, stripes = 8, 16, 3072 + 16, 3
-    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=91)
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=91, policy=policy)
     try:
         st.encode()
         ids = [1, 2, 5, 6, 9, 10, 13, 15]
@@ -583,7 +595,7 @@ def test_decode_dynamic_schedule_concurrent_streams_and_tiny():
     k, n = 8, 16
     ids = [0, 1, 4, 5, 9, 12, 14, 15]
     for S, stripes in ((64 * 1024, 6), (16, 1), (1024 + 16, 3)):
-        st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=21)
+        st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=21, policy=pm.PMRC_PLAN_JIT)
         try:
             st.encode()
             assert "atomicAdd(dctr" in pm.pmrc_plan_source(st.code, 0, 0, ids)
@@ -608,7 +620,7 @@ def test_independent_launches_per_stripe_repair_and_decode():
     # config 4's per-stripe patterns with consecutive launches declared independent (programmatic
     # dependent launch: a launch's CTAs start while the previous launch's CTAs retire)
     k, n, S, stripes = 8, 16, 64 * 1024, 6
-    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=31)
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=31, policy=pm.PMRC_PLAN_JIT)
     try:
         st.encode()
         pm.pmrc_set_independent_launches(st.code, 1)

@@ -193,6 +193,21 @@ int pmrc_decode_batch(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_
 int pmrc_repair_batch(pmrc_code *c, const int *lost_ids, const int *helper_ids, int n_helpers, const pmrc_cregion *nodes,
                       pmrc_region out_piece, size_t S, size_t stripes, void *stream);
 
+/* The paper's "specific" product-matrix decoders, for the
+ * linear-vs-specific comparison: from exactly k survivors, MSR codes run the
+ * symmetric-matrix method (A = C_DC Phi_DC^t; P, Q from its off-diagonal pairs; U = P/Q rows times
+ * the other survivors' (Phi^t)^-1; S1, S2 = Phi_sel^-1 U_sel; the message Z through L) and then the
+ * systematic data X_miss = Gtilde[miss] Z; MBR codes run T = Phi_DC^-1 R_right,
+ * W = R_left + Delta_DC T^t, S = Phi_DC^-1 W, X through L.  Each step is one launch of a region
+ * linear combination (on the engine pmrc_set_plan_policy selects) with its blocks in `scratch`
+ * (device memory of at least pmrc_decode_specific_scratch bytes, caller-owned).  Output contract as
+ * pmrc_decode: only the data blocks no surviving systematic node holds are written, and the result
+ * equals pmrc_decode's (the decoded data is unique).  PMRC_EINVAL unless n_surv == k;
+ * PMRC_EUNSUPPORTED for RS and GF(2^16) codes; PMRC_ESINGULAR for a singular submatrix. */
+int pmrc_decode_specific_scratch(pmrc_code *c, size_t S, size_t stripes, size_t *bytes);
+int pmrc_decode_specific(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_cregion *pieces, void *data_out,
+                         void *scratch, size_t scratch_bytes, size_t S, size_t stripes, int *n_written, void *stream);
+
 /* Cap the grid of every launch on this handle at max_ctas CTAs (0 = default: one full wave, one
  * persistent CTA per SM).  With a cap, small launches issued on several streams (e.g. config 4's
  * per-stripe failure patterns, one plan per stripe) run side by side on disjoint SMs instead of

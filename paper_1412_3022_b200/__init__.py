@@ -25,7 +25,7 @@ EXPORTS = ["pmrc_create", "pmrc_destroy", "pmrc_info", "pmrc_matrix", "pmrc_layo
            "pmrc_read_cost", "pmrc_launch_count", "pmrc_strerror", "pmrc_last_error", "pmrc_precompile",
            "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source", "pmrc_plan_stats", "pmrc_apply", "pmrc_apply_stats", "pmrc_set_max_ctas",
            "pmrc_set_independent_launches", "pmrc_set_plan_policy", "pmrc_get_plan_policy", "pmrc_plan_prepare",
-           "pmrc_decode_batch", "pmrc_repair_batch"]
+           "pmrc_decode_batch", "pmrc_repair_batch", "pmrc_decode_specific", "pmrc_decode_specific_scratch"]
 
 
 class PmrcError(RuntimeError):
@@ -97,6 +97,8 @@ def lib():
             "pmrc_plan_prepare": ([P, I, I, IP, I], I),
             "pmrc_decode_batch": ([P, IP, I, ctypes.POINTER(pmrc_cregion), P, Z, Z, IP, P], I),
             "pmrc_repair_batch": ([P, IP, IP, I, ctypes.POINTER(pmrc_cregion), pmrc_region, Z, Z, P], I),
+            "pmrc_decode_specific_scratch": ([P, Z, Z, ctypes.POINTER(ctypes.c_size_t)], I),
+            "pmrc_decode_specific": ([P, IP, I, ctypes.POINTER(pmrc_cregion), P, P, Z, Z, Z, IP, P], I),
             "pmrc_strerror": ([I], ctypes.c_char_p),
             "pmrc_last_error": ([], ctypes.c_char_p),
         }
@@ -283,6 +285,24 @@ def pmrc_repair_batch(code, lost_ids, helper_ids, nodes, out_piece, S, stripes, 
     regs = (pmrc_cregion * max(1, len(nodes)))(*[pmrc_cregion(p, s) for p, s in nodes])
     _check(lib().pmrc_repair_batch(code, lost, ids, nh, regs, pmrc_region(*out_piece), S, stripes, stream),
            "pmrc_repair_batch")
+
+
+def pmrc_decode_specific_scratch(code, S, stripes):
+    """Bytes of device scratch pmrc_decode_specific needs for (S, stripes)."""
+    n = ctypes.c_size_t()
+    _check(lib().pmrc_decode_specific_scratch(code, S, stripes, ctypes.byref(n)), "pmrc_decode_specific_scratch")
+    return n.value
+
+
+def pmrc_decode_specific(code, surv_ids, pieces, data_out_ptr, scratch_ptr, scratch_bytes, S, stripes, stream=0):
+    """The paper's specific MSR / MBR decoder from exactly k survivors (pieces: (ptr, stride) each).
+    Returns blocks written per stripe."""
+    ids, n = _ints(surv_ids)
+    regs = (pmrc_cregion * max(1, n))(*[pmrc_cregion(p, s) for p, s in pieces])
+    nw = ctypes.c_int()
+    _check(lib().pmrc_decode_specific(code, ids, n, regs, data_out_ptr, scratch_ptr, scratch_bytes, S, stripes,
+                                      ctypes.byref(nw), stream), "pmrc_decode_specific")
+    return nw.value
 
 
 def pmrc_apply_stats(code, A):

@@ -287,7 +287,7 @@ int apply_gen_knobs(const std::string &s, GenOptions &G, std::string &err) {
 
 }  // namespace
 
-static int get_rt_plan(pmrc_code *c, const std::string &key, const PlanSpec &spec, int R, RtPlan **out);
+static int get_rt_plan(pmrc_code *c, const std::string &key, const PlanSpec &spec, int R, int G, RtPlan **out);
 
 extern "C" {
 
@@ -562,7 +562,7 @@ int pmrc_encode(pmrc_code *c, const void *data, void *parity, size_t S, size_t s
     // the same G'' on the runtime-coefficient kernel (the formulation comparison of DESIGN.md)
     const pmrc_rt::RlcShape sh = rt_shape(D.P, c->gen);
     RtPlan *P = nullptr;
-    rc = get_rt_plan(c, "enc", c->enc_spec, sh.R, &P);
+    rc = get_rt_plan(c, "enc", c->enc_spec, sh.R, sh.G, &P);
     if (rc) return rc;
     rc = ensure_device(c);
     if (rc) return rc;
@@ -935,11 +935,13 @@ static bool use_runtime(const pmrc_code *c, const std::string &key) {
   return !c->plans.count(key);
 }
 
-static std::string rt_key(const std::string &key, int R) { return key + "#rt" + std::to_string(R); }
+static std::string rt_key(const std::string &key, int R, int G) {
+  return key + "#rt" + std::to_string(R) + "x" + std::to_string(G);
+}
 
-// runtime plan of `spec` for R-row blocks, cached on the handle under `key`
-static int get_rt_plan(pmrc_code *c, const std::string &key, const PlanSpec &spec, int R, RtPlan **out) {
-  const std::string k = rt_key(key, R);
+// runtime plan of `spec` for R-row blocks and G row groups, cached on the handle under `key`
+static int get_rt_plan(pmrc_code *c, const std::string &key, const PlanSpec &spec, int R, int G, RtPlan **out) {
+  const std::string k = rt_key(key, R, G);
   auto it = c->rt_plans.find(k);
   if (it != c->rt_plans.end()) {
     *out = it->second.get();
@@ -947,7 +949,7 @@ static int get_rt_plan(pmrc_code *c, const std::string &key, const PlanSpec &spe
   }
   auto p = std::make_unique<RtPlan>();
   std::string err;
-  int rc = rt_build(spec, R, *p, err);
+  int rc = rt_build(spec, R, G, *p, err);
   if (rc) return fail(rc, err);
   *out = p.get();
   c->rt_plans[k] = std::move(p);
@@ -993,7 +995,7 @@ static int run_plan(pmrc_code *c, const std::string &key, const PlanSpec &spec, 
   if (use_runtime(c, key)) {
     const pmrc_rt::RlcShape sh = rt_shape((int)spec.outputs.size(), c->gen);
     RtPlan *P = nullptr;
-    int rc = get_rt_plan(c, key, spec, sh.R, &P);
+    int rc = get_rt_plan(c, key, spec, sh.R, sh.G, &P);
     if (rc == PMRC_OK) {
       if (!stripes || !S) return PMRC_OK;
       rc = ensure_device(c);
@@ -1298,7 +1300,7 @@ static int run_batch(pmrc_code *c, const std::vector<std::string> &keys, const s
     if (it == idx.end()) {
       if (plans.size() >= 0xFFFF) return fail(PMRC_EUNSUPPORTED, "too many distinct patterns in one batch");
       RtPlan *P = nullptr;
-      int rc = get_rt_plan(c, keys[t], *specs[t], sh.R, &P);
+      int rc = get_rt_plan(c, keys[t], *specs[t], sh.R, sh.G, &P);
       if (rc) return rc;
       it = idx.insert({keys[t], (uint16_t)plans.size()}).first;
       plans.push_back(P);
@@ -1388,6 +1390,306 @@ int pmrc_repair_batch(pmrc_code *c, const int *lost_ids, const int *helper_ids, 
   if (rc) return fail(rc, "bad region");
   return run_batch(c, keys, specs, nodes, (uint64_t)(uintptr_t)out_piece.ptr, out_piece.stripe_stride, S, stripes,
                    stream);
+}
+
+// ---------------------------------------------------------------------------------------------
+// The paper's "specific" product-matrix decoders (NEXT-2) on the
+// GPU: each algebraic step is one region linear combination (a plan on the same engines), with the
+// intermediate blocks in caller scratch.  Exactly k survivors (the decoders' data collector).
+//   MSR:  A = C_DC Phi_DC^t;  Q_ij = (A_ij + A_ji)/(l_i + l_j),  P_ij = A_ij + l_i Q_ij
+//                 (i != j);  U1_i = (P row i, off-diagonal) (Phi_others(i)^t)^-1, U2_i likewise
+//                 from Q;  S1 = Phi_sel^-1 U1_sel,  S2 = Phi_sel^-1 U2_sel  (sel = first alpha
+//                 survivors);  Z through L;  systematic data  X_miss = Gtilde[miss] Z
+//   MBR:  T = Phi_DC^-1 R_right;  W = R_left + Delta_DC T^t;  S = Phi_DC^-1 W;  X through
+//                 L (only the blocks no surviving systematic node holds are written)
+// Slots: 0..k-1 survivor pieces, k.. scratch stage buffers, last = data_out.
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+struct SpecStages {
+  std::vector<PlanSpec> stages;
+  std::vector<int> scratch_blocks;  // blocks per stripe of each scratch buffer (slot k + b)
+  int written = 0;                  // data blocks written per stripe
+};
+
+int msr_specific_stages(const pmrc_code *c, const int *ids, SpecStages &out) {
+  const CodeDef &D = c->def;
+  const GF256 &F = gf();
+  const int k = D.k, a = D.alpha, d = D.d, B = D.B;
+  if (k - 1 != a) return PMRC_EUNSUPPORTED;
+  auto phi = [&](int node, int t) { return D.psi.at(node, t); };
+  for (int x = 0; x < k; x++)
+    for (int y = 0; y < x; y++)
+      if (D.lambda[ids[x]] == D.lambda[ids[y]]) return PMRC_ESINGULAR;
+  // per-survivor inverse of the other survivors' Phi^t, and Phi_sel^-1
+  std::vector<Mat> oth(k);
+  for (int i = 0; i < k; i++) {
+    Mat M(a, a);
+    int r = 0;
+    for (int j = 0; j < k; j++) {
+      if (j == i) continue;
+      for (int t = 0; t < a; t++) M.at(t, r) = phi(ids[j], t);
+      r++;
+    }
+    if (!invert(M, oth[i])) return PMRC_ESINGULAR;
+  }
+  Mat Sel(a, a), SelInv;
+  for (int x = 0; x < a; x++)
+    for (int t = 0; t < a; t++) Sel.at(x, t) = phi(ids[x], t);
+  if (!invert(Sel, SelInv)) return PMRC_ESINGULAR;
+  const int sA = k, sPQ = k + 1, sU = k + 2, sZ = k + 3, sOut = k + 4, nslots = k + 5;
+  out.scratch_blocks = {k * k, 2 * k * k, 2 * k * a, B};
+  // stage 1: A_ij = sum_t phi_j[t] C_i[t]
+  PlanSpec s1;
+  s1.n_slots = nslots;
+  for (int i = 0; i < k; i++)
+    for (int t = 0; t < a; t++) s1.inputs.push_back({{{i, t, 1}}});
+  for (int i = 0; i < k; i++)
+    for (int j = 0; j < k; j++) s1.outputs.push_back({sA, i * k + j});
+  s1.A = Mat(k * k, k * a);
+  for (int i = 0; i < k; i++)
+    for (int j = 0; j < k; j++)
+      for (int t = 0; t < a; t++) s1.A.at(i * k + j, i * a + t) = phi(ids[j], t);
+  // stage 2: P_ij, Q_ij (i != j) from A_ij, A_ji
+  PlanSpec s2;
+  s2.n_slots = nslots;
+  for (int e = 0; e < k * k; e++) s2.inputs.push_back({{{sA, e, 1}}});
+  std::vector<std::pair<int, int>> offd;
+  for (int i = 0; i < k; i++)
+    for (int j = 0; j < k; j++)
+      if (i != j) offd.push_back({i, j});
+  s2.A = Mat(2 * (int)offd.size(), k * k);
+  for (size_t q = 0; q < offd.size(); q++) {
+    const int i = offd[q].first, j = offd[q].second;
+    const uint8_t li = D.lambda[ids[i]], lj = D.lambda[ids[j]];
+    const uint8_t cq = F.inv(li ^ lj);
+    s2.outputs.push_back({sPQ, 2 * (i * k + j)});      // P_ij
+    s2.outputs.push_back({sPQ, 2 * (i * k + j) + 1});  // Q_ij
+    const uint8_t lc = F.mul(li, cq);
+    s2.A.at(2 * (int)q, i * k + j) = 1 ^ lc;           // P_ij = (1 + l_i c) A_ij + l_i c A_ji
+    s2.A.at(2 * (int)q, j * k + i) = lc;
+    s2.A.at(2 * (int)q + 1, i * k + j) = cq;           // Q_ij = c (A_ij + A_ji)
+    s2.A.at(2 * (int)q + 1, j * k + i) = cq;
+  }
+  // stage 3: U1_i = P_i,others . oth_i, U2_i = Q_i,others . oth_i
+  PlanSpec s3;
+  s3.n_slots = nslots;
+  for (int e = 0; e < 2 * k * k; e++) s3.inputs.push_back({{{sPQ, e, 1}}});
+  s3.A = Mat(2 * k * a, 2 * k * k);
+  for (int w = 0; w < 2; w++)
+    for (int i = 0; i < k; i++)
+      for (int cc = 0; cc < a; cc++) {
+        const int row = w * k * a + i * a + cc;
+        s3.outputs.push_back({sU, row});
+        int r = 0;
+        for (int j = 0; j < k; j++) {
+          if (j == i) continue;
+          s3.A.at(row, 2 * (i * k + j) + w) = oth[i].at(r, cc);
+          r++;
+        }
+      }
+  // stage 4: S1 = SelInv U1_sel, S2 = SelInv U2_sel, written as Z through L (each index once)
+  PlanSpec s4;
+  s4.n_slots = nslots;
+  for (int e = 0; e < 2 * k * a; e++) s4.inputs.push_back({{{sU, e, 1}}});
+  std::vector<char> done(B + 1, 0);
+  std::vector<std::vector<uint8_t>> rows4;
+  for (int l = 0; l < d; l++)
+    for (int j = 0; j < a; j++) {
+      const int idx = D.Lidx[(size_t)l * D.Lcols + j];
+      if (idx <= 0 || done[idx]) continue;
+      done[idx] = 1;
+      const int w = l < a ? 0 : 1, rr = l < a ? l : l - a;  // S_w[rr][j]
+      std::vector<uint8_t> row(2 * k * a, 0);
+      for (int t = 0; t < a; t++) row[w * k * a + t * a + j] = SelInv.at(rr, t);
+      s4.outputs.push_back({sZ, idx - 1});
+      rows4.push_back(row);
+    }
+  s4.A = Mat((int)rows4.size(), 2 * k * a);
+  for (size_t r = 0; r < rows4.size(); r++) memcpy(&s4.A.a[r * 2 * k * a], rows4[r].data(), 2 * k * a);
+  // stage 5: X_miss = Gtilde[miss] Z  (Gtilde = G's first B rows)
+  std::vector<char> held(B, 0);
+  for (int x = 0; x < k; x++)
+    if (ids[x] < k)
+      for (int j = 0; j < a; j++) held[D.sys_block(ids[x], j)] = 1;
+  std::vector<int> miss;
+  for (int m = 0; m < B; m++)
+    if (!held[m]) miss.push_back(m);
+  out.written = (int)miss.size();
+  out.stages = {s1, s2, s3, s4};
+  if (miss.empty()) return PMRC_OK;
+  PlanSpec s5;
+  s5.n_slots = nslots;
+  std::vector<int> used;
+  for (int z = 0; z < B; z++) {
+    bool nz = false;
+    for (int m : miss) nz |= D.G.at(m, z) != 0;
+    if (nz) used.push_back(z);
+  }
+  for (int z : used) s5.inputs.push_back({{{sZ, z, 1}}});
+  for (int m : miss) s5.outputs.push_back({sOut, m});
+  s5.A = Mat((int)miss.size(), (int)used.size());
+  for (size_t r = 0; r < miss.size(); r++)
+    for (size_t x = 0; x < used.size(); x++) s5.A.at((int)r, (int)x) = D.G.at(miss[r], used[x]);
+  out.stages.push_back(s5);
+  return PMRC_OK;
+}
+
+int mbr_specific_stages(const pmrc_code *c, const int *ids, SpecStages &out) {
+  const CodeDef &D = c->def;
+  const int k = D.k, d = D.d, B = D.B, dk = d - k;
+  Mat Phi(k, k), PhiInv;
+  for (int x = 0; x < k; x++)
+    for (int t = 0; t < k; t++) Phi.at(x, t) = D.psi.at(ids[x], t);
+  if (!invert(Phi, PhiInv)) return PMRC_ESINGULAR;
+  const int sT = k, sW = k + 1, sOut = k + 2, nslots = k + 3;
+  out.scratch_blocks = {std::max(1, k * dk), k * k};
+  std::vector<PlanSpec> st;
+  // stage 1: T[r][cc] = sum_t PhiInv[r][t] R[t][k + cc]
+  if (dk > 0) {
+    PlanSpec s1;
+    s1.n_slots = nslots;
+    for (int t = 0; t < k; t++)
+      for (int cc = 0; cc < dk; cc++) s1.inputs.push_back({{{t, k + cc, 1}}});
+    s1.A = Mat(k * dk, k * dk);
+    for (int r = 0; r < k; r++)
+      for (int cc = 0; cc < dk; cc++) {
+        s1.outputs.push_back({sT, r * dk + cc});
+        for (int t = 0; t < k; t++) s1.A.at(r * dk + cc, t * dk + cc) = PhiInv.at(r, t);
+      }
+    st.push_back(s1);
+  }
+  // stage 2: W[x][cc] = R[x][cc] + sum_t Delta[x][t] T[cc][t]
+  PlanSpec s2;
+  s2.n_slots = nslots;
+  for (int x = 0; x < k; x++)
+    for (int cc = 0; cc < k; cc++) s2.inputs.push_back({{{x, cc, 1}}});
+  for (int e = 0; e < k * dk; e++) s2.inputs.push_back({{{sT, e, 1}}});
+  s2.A = Mat(k * k, k * k + k * dk);
+  for (int x = 0; x < k; x++)
+    for (int cc = 0; cc < k; cc++) {
+      s2.outputs.push_back({sW, x * k + cc});
+      s2.A.at(x * k + cc, x * k + cc) = 1;
+      for (int t = 0; t < dk; t++) s2.A.at(x * k + cc, k * k + cc * dk + t) = D.psi.at(ids[x], k + t);
+    }
+  st.push_back(s2);
+  // stage 3: S = PhiInv W (missing blocks only), T entries of missing blocks copied from T
+  std::vector<char> held(B, 0);
+  for (int x = 0; x < k; x++)
+    if (ids[x] < k)
+      for (int j = 0; j < d; j++) held[D.sys_block(ids[x], j)] = 1;
+  PlanSpec s3;
+  s3.n_slots = nslots;
+  for (int e = 0; e < k * k; e++) s3.inputs.push_back({{{sW, e, 1}}});
+  for (int e = 0; e < k * dk; e++) s3.inputs.push_back({{{sT, e, 1}}});
+  std::vector<char> done(B + 1, 0);
+  std::vector<std::vector<uint8_t>> rows3;
+  for (int r = 0; r < k; r++)
+    for (int cc = 0; cc < d; cc++) {
+      const int idx = D.Lidx[(size_t)r * D.Lcols + cc];
+      if (idx <= 0 || done[idx] || held[idx - 1]) continue;
+      done[idx] = 1;
+      std::vector<uint8_t> row(k * k + k * dk, 0);
+      if (cc < k) {
+        for (int t = 0; t < k; t++) row[t * k + cc] = PhiInv.at(r, t);  // S[r][cc]
+      } else {
+        row[k * k + r * dk + (cc - k)] = 1;                             // T[r][cc - k]
+      }
+      s3.outputs.push_back({sOut, idx - 1});
+      rows3.push_back(row);
+    }
+  out.written = (int)rows3.size();
+  if (!rows3.empty()) {
+    s3.A = Mat((int)rows3.size(), k * k + k * dk);
+    for (size_t r = 0; r < rows3.size(); r++) memcpy(&s3.A.a[r * (k * k + k * dk)], rows3[r].data(), k * k + k * dk);
+    st.push_back(s3);
+  }
+  out.stages = st;
+  return PMRC_OK;
+}
+
+int specific_stages(const pmrc_code *c, const int *ids, SpecStages &out) {
+  if (c->w != 8) return PMRC_EUNSUPPORTED;
+  const int kind = c->def.kind;
+  if (kind == KIND_MBR) return mbr_specific_stages(c, ids, out);
+  if (kind == KIND_RS) return PMRC_EUNSUPPORTED;
+  return msr_specific_stages(c, ids, out);
+}
+
+size_t scratch_bytes_of(const SpecStages &ss, size_t S, size_t stripes) {
+  size_t t = 0;
+  for (int b : ss.scratch_blocks) t += (size_t)b * S * stripes;
+  return t;
+}
+
+}  // namespace
+
+int pmrc_decode_specific_scratch(pmrc_code *c, size_t S, size_t stripes, size_t *bytes) {
+  if (!c || !bytes) return fail(PMRC_EINVAL, "NULL argument");
+  const CodeDef &D = c->def;
+  std::vector<int> ids(D.k);
+  for (int i = 0; i < D.k; i++) ids[i] = D.n - D.k + i;  // shape only (any k-set has the same buffers)
+  SpecStages ss;
+  int rc = specific_stages(c, ids.data(), ss);
+  if (rc == PMRC_ESINGULAR) {  // the scratch shape does not depend on the set: use the first k nodes
+    for (int i = 0; i < D.k; i++) ids[i] = i;
+    rc = specific_stages(c, ids.data(), ss);
+  }
+  if (rc) return fail(rc, "specific decoder: unsupported code");
+  *bytes = scratch_bytes_of(ss, S, stripes);
+  return PMRC_OK;
+}
+
+int pmrc_decode_specific(pmrc_code *c, const int *surv_ids_in, int n_surv, const pmrc_cregion *pieces_in,
+                         void *data_out, void *scratch, size_t scratch_bytes, size_t S, size_t stripes,
+                         int *n_written, void *stream) {
+  if (n_written) *n_written = 0;
+  if (!c || !surv_ids_in || !pieces_in || !data_out || !scratch) return fail(PMRC_EINVAL, "NULL argument");
+  const CodeDef &D = c->def;
+  if (n_surv != D.k || check_ids(D, surv_ids_in, n_surv)) return fail(PMRC_EINVAL, "specific decode needs exactly k distinct survivors");
+  if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
+  std::vector<int> surv;
+  std::vector<pmrc_cregion> pieces;
+  canonical_order(surv_ids_in, pieces_in, n_surv, surv, pieces);
+  SpecStages ss;
+  int rc = specific_stages(c, surv.data(), ss);
+  if (rc) return fail(rc, rc == PMRC_ESINGULAR ? "specific decoder: singular submatrix for this survivor set"
+                                               : "specific decoder: unsupported code (MSR / MBR over GF(2^8))");
+  if (n_written) *n_written = ss.written;
+  if (!stripes || !S) return PMRC_OK;
+  if (scratch_bytes < scratch_bytes_of(ss, S, stripes)) return fail(PMRC_EINVAL, "scratch too small");
+  const int k = D.k, nb = (int)ss.scratch_blocks.size(), nslots = k + nb + 1;
+  std::vector<uint64_t> ptrs(nslots), strides(nslots);
+  for (int a = 0; a < k; a++) {
+    rc = check_region(pieces[a].ptr, pieces[a].stripe_stride, stripes);
+    if (rc) return fail(rc, "bad survivor piece region");
+    ptrs[a] = (uint64_t)(uintptr_t)pieces[a].ptr;
+    strides[a] = pieces[a].stripe_stride;
+  }
+  rc = check_region(scratch, 16, stripes);
+  if (!rc) rc = check_region(data_out, (size_t)D.B * S, stripes);
+  if (rc) return fail(rc, "bad scratch / data_out");
+  uint64_t off = (uint64_t)(uintptr_t)scratch;
+  for (int b = 0; b < nb; b++) {
+    ptrs[k + b] = off;
+    strides[k + b] = (uint64_t)ss.scratch_blocks[b] * S;
+    off += (uint64_t)ss.scratch_blocks[b] * S * stripes;
+  }
+  ptrs[k + nb] = (uint64_t)(uintptr_t)data_out;
+  strides[k + nb] = (uint64_t)D.B * S;
+  const std::string base = ids_key("spec", surv.data(), n_surv, 0);
+  for (size_t q = 0; q < ss.stages.size(); q++) {
+    const std::string key = base + ":" + std::to_string(q);
+    const PlanSpec *sp = nullptr;
+    rc = get_spec(c, key, [&](PlanSpec &x) {
+      x = ss.stages[q];
+      return PMRC_OK;
+    }, &sp);
+    if (rc) return rc;
+    rc = run_plan(c, key, *sp, ptrs.data(), strides.data(), S, stripes, stream);
+    if (rc) return rc;
+  }
+  return PMRC_OK;
 }
 
 int pmrc_plan_prepare(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstring>
 
 #include "../../../include/pmrc.h"
@@ -46,7 +47,7 @@ static void tables(uint8_t c, uint32_t *a4, uint32_t *b1) {
   *b1 = pk(t2);
 }
 
-int rt_build(const PlanSpec &p, int R, RtPlan &out, std::string &err) {
+int rt_build(const PlanSpec &p, int R, int G, RtPlan &out, std::string &err) {
   if (p.w != 8) {
     err = "runtime-coefficient kernel: GF(2^8) plans only";
     return PMRC_EUNSUPPORTED;
@@ -62,9 +63,47 @@ int rt_build(const PlanSpec &p, int R, RtPlan &out, std::string &err) {
     err = "runtime-coefficient kernel: bad plan size";
     return PMRC_EUNSUPPORTED;
   }
-  const int n_rb = (n_out + R - 1) / R;  // row blocks of R rows (a pass runs G of them)
-  // layout (words): header 16 | tabA 4*n_in*n_out | ttabA 4*n_terms | tabB n_in*n_out | ttabB n_terms |
-  //                 terms 2*n_terms | outs 2*n_out | masks n_in*n_rb      (16-B aligned uint4 arrays first)
+  const int n_rb = (n_out + R - 1) / R;  // row blocks of R rows
+  const int n_pass = (n_rb + G - 1) / G; // a pass runs G row blocks
+  // row order: rows of equal support side by side, densest first (sparse MSR encode: the n-k rows
+  // of a PM symbol index share their support, so every R-row block is all or nothing per input);
+  // the kernel runs a block without per-row branches when every row of it reads the input
+  std::vector<int> ord(n_out);
+  for (int r = 0; r < n_out; r++) ord[r] = r;
+  {
+    std::vector<std::vector<uint8_t>> sup(n_out, std::vector<uint8_t>(n_in));
+    std::vector<int> cnt(n_out, 0);
+    for (int r = 0; r < n_out; r++)
+      for (int i = 0; i < n_in; i++) cnt[r] += (sup[r][i] = p.A.at(r, i) != 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+      if (cnt[x] != cnt[y]) return cnt[x] > cnt[y];
+      return sup[x] > sup[y];
+    });
+  }
+  std::vector<uint32_t> masks((size_t)n_in * n_rb, 0u);
+  long nnz = 0;
+  for (int i = 0; i < n_in; i++)
+    for (int r = 0; r < n_out; r++)
+      if (p.A.at(ord[r], i)) {
+        nnz++;
+        masks[(size_t)i * n_rb + r / R] |= 1u << (r % R);
+      }
+  // pass sequences: pass pp streams every term of each input that a row of its G row blocks reads
+  std::vector<int> tstart(n_in + 1, 0);
+  for (int i = 0; i < n_in; i++) tstart[i + 1] = tstart[i] + (int)p.inputs[i].terms.size();
+  std::vector<uint32_t> pstart(n_pass + 1, 0), seq;
+  for (int pp = 0; pp < n_pass; pp++) {
+    pstart[pp] = (uint32_t)seq.size();
+    for (int i = 0; i < n_in; i++) {
+      bool used = false;
+      for (int rb = pp * G; rb < std::min(n_rb, pp * G + G); rb++) used |= masks[(size_t)i * n_rb + rb] != 0;
+      if (used)
+        for (int q = tstart[i]; q < tstart[i + 1]; q++) seq.push_back((uint32_t)q);
+    }
+  }
+  pstart[n_pass] = (uint32_t)seq.size();
+  // layout (words): header | ttabA 4*n_terms | ttabB n_terms | terms 2*n_terms | outs 2*n_out |
+  //                 masks n_in*n_rb | pstart n_pass+1 | seq | (16-B aligned) tabA 4*n_in*n_out | tabB n_in*n_out
   RlcHdr h = {};
   h.magic = pmrc_rt::kRlcMagic;
   h.n_in = n_in;
@@ -72,7 +111,10 @@ int rt_build(const PlanSpec &p, int R, RtPlan &out, std::string &err) {
   h.n_terms = n_terms;
   h.R = R;
   h.n_rb = n_rb;
-  uint32_t w = 16;
+  h.G = G;
+  h.n_pass = n_pass;
+  h.seq_len = (uint32_t)seq.size();
+  uint32_t w = sizeof(RlcHdr) / 4;
   h.off_ttabA = w;
   w += 4u * n_terms;
   h.off_ttabB = w;
@@ -82,7 +124,11 @@ int rt_build(const PlanSpec &p, int R, RtPlan &out, std::string &err) {
   h.off_outs = w;
   w += 2u * n_out;
   h.off_masks = w;
-  w += (uint32_t)n_in * n_rb;
+  w += (uint32_t)masks.size();
+  h.off_pstart = w;
+  w += (uint32_t)pstart.size();
+  h.off_seq = w;
+  w += (uint32_t)seq.size();
   w = (w + 3u) & ~3u;  // tabA is read as uint4
   h.off_tabA = w;
   w += 4u * n_in * n_out;
@@ -99,32 +145,15 @@ int rt_build(const PlanSpec &p, int R, RtPlan &out, std::string &err) {
       return PMRC_EUNSUPPORTED;
     }
   }
-  // row order: rows of equal support side by side, densest first (sparse MSR encode: the n-k rows
-  // of a PM symbol index share their support, so every R-row block is all or nothing per input);
-  // the kernel runs a block without per-row branches when every row of it reads the input
-  std::vector<int> ord(n_out);
-  for (int r = 0; r < n_out; r++) ord[r] = r;
-  {
-    std::vector<std::vector<uint8_t>> sup(n_out, std::vector<uint8_t>(n_in));
-    std::vector<int> cnt(n_out, 0);
-    for (int r = 0; r < n_out; r++)
-      for (int i = 0; i < n_in; i++) cnt[r] += (sup[r][i] = p.A.at(r, i) != 0);
-    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
-      if (cnt[x] != cnt[y]) return cnt[x] > cnt[y];
-      return sup[x] > sup[y];
-    });
-  }
   std::vector<uint32_t> b(w, 0u);
-  long nnz = 0;
   for (int i = 0; i < n_in; i++)
     for (int r = 0; r < n_out; r++) {
       const uint8_t c = p.A.at(ord[r], i);
-      if (!c) continue;
-      nnz++;
-      const size_t e = (size_t)i * n_out + r;
-      tables(c, &b[h.off_tabA + 4 * e], &b[h.off_tabB + e]);
-      b[h.off_masks + (size_t)i * n_rb + r / R] |= 1u << (r % R);
+      if (c) tables(c, &b[h.off_tabA + 4 * ((size_t)i * n_out + r)], &b[h.off_tabB + (size_t)i * n_out + r]);
     }
+  std::copy(masks.begin(), masks.end(), b.begin() + h.off_masks);
+  std::copy(pstart.begin(), pstart.end(), b.begin() + h.off_pstart);
+  std::copy(seq.begin(), seq.end(), b.begin() + h.off_seq);
   int q = 0;
   for (int i = 0; i < n_in; i++) {
     const auto &terms = p.inputs[i].terms;
@@ -155,6 +184,7 @@ int rt_build(const PlanSpec &p, int R, RtPlan &out, std::string &err) {
   rt_free(out);
   out.blob = std::move(b);
   out.R = R;
+  out.G = G;
   out.n_in = n_in;
   out.n_out = n_out;
   out.n_terms = n_terms;
@@ -188,12 +218,12 @@ int rt_launch(const std::vector<RtPlan *> &plans, const uint16_t *stripe_plan, c
   unsigned max_words = 0;
   bool tg = false;
   for (RtPlan *p : plans) {
-    tg |= (p->blob[7] & pmrc_rt::kRlcGlobalTables) != 0;
-    if (p->R != sh.R) {
+    tg |= (p->blob[offsetof(RlcHdr, flags) / 4] & pmrc_rt::kRlcGlobalTables) != 0;
+    if (p->R != sh.R || (int)p->blob[offsetof(RlcHdr, G) / 4] != sh.G) {
       err = "rt_launch: plans of one launch must share their shape";
       return PMRC_EINVAL;
     }
-    max_words = std::max(max_words, p->blob[15]);  // smem_words
+    max_words = std::max(max_words, p->blob[offsetof(RlcHdr, smem_words) / 4]);
     if (!p->dev) {
       const size_t nb = p->blob.size() * 4;
       if (cudaMalloc(&p->dev, nb) != cudaSuccess) {

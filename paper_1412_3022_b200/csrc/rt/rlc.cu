@@ -43,6 +43,7 @@
 //     changes, so config 4's per-stripe failure patterns run in ONE launch (stripe_plan[t]); the
 //     coefficient tables of larger plans (k = 16 decode: 1.1 MB) are read from device memory (TG).
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include "rlc.hpp"
@@ -186,8 +187,7 @@ __global__ void __launch_bounds__(GT * G + 32, G == 1 ? 2 : 1) rlc_kernel(const 
       const u32 pi = a.stripe_plan ? (u32)a.stripe_plan[t] : 0u;
       if (pi == 0xFFFFu) return 0u;
       pb = a.stripe_plan ? (const u32 *)a.plan_ptrs[pi] : a.plan0;
-      const u32 n_terms = __ldg(pb + 4), n_rb = __ldg(pb + 6);
-      return ((n_rb + G - 1) / G) * n_terms;
+      return __ldg(pb + offsetof(RlcHdr, seq_len) / 4);
     };
     u64 it = i0;   // walk position (uniform): item and offset within it
     u32 e = 0;
@@ -207,13 +207,13 @@ __global__ void __launch_bounds__(GT * G + 32, G == 1 ? 2 : 1) rlc_kernel(const 
       if (k >= (u32)D) mbar_wait(bar_empty + 8 * s, ((k / D) - 1) & 1);
       if (mine) {
         const u64 t = itj / tiles, tile = itj - t * tiles;
-        const u32 n_terms = __ldg(pb + 4), n_rb = __ldg(pb + 6), off_terms = __ldg(pb + 12);
-        const u32 j = ej % n_terms;
+        const u32 n_pass = __ldg(pb + offsetof(RlcHdr, n_pass) / 4), off_terms = __ldg(pb + offsetof(RlcHdr, off_terms) / 4);
+        const u32 j = __ldg(pb + __ldg(pb + offsetof(RlcHdr, off_seq) / 4) + ej);
         const u64 p0 = tile * TP;
         const u32 bytes = (u32)((a.S - p0) < TP ? (a.S - p0) : TP);
-        // single-pass plans read each tile once: stream it (evict-first); multi-pass plans re-read
-        // the tile once per pass, from L2
-        const u64 pol = (n_rb + G - 1) / G == 1 ? pol_first : pol_normal;
+        // single-pass plans read each tile once: stream it (evict-first); multi-pass plans may
+        // re-read it in a later pass, from L2
+        const u64 pol = n_pass == 1 ? pol_first : pol_normal;
         const u32 w0 = __ldg(pb + off_terms + 2 * j), w1 = __ldg(pb + off_terms + 2 * j + 1);
         const u32 slot = w0 & 0xFFFFu, blk = w1 & 0xFFFFu;
         const unsigned char *src =
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(GT * G + 32, G == 1 ? 2 : 1) rlc_kernel(const 
     if (pl != cur) {             // (re)load the stripe's plan into shared memory
       named_sync(1, NCT);
       const u32 *src = a.stripe_plan ? (const u32 *)a.plan_ptrs[pl] : a.plan0;
-      const u32 words = __ldg(src + 15);  // smem_words
+      const u32 words = __ldg(src + offsetof(RlcHdr, smem_words) / 4);
       for (u32 e = threadIdx.x * 4; e < words; e += NCT * 4) {
         if (e + 4 <= words) *(uint4 *)(sm + e) = __ldg((const uint4 *)(src + e));
         else
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(GT * G + 32, G == 1 ? 2 : 1) rlc_kernel(const 
       h = *(const RlcHdr *)sm;
       tabs = TG ? src : sm;
     }
-    const u32 n_rb = h.n_rb, passes = (n_rb + G - 1) / G;
+    const u32 n_rb = h.n_rb, passes = h.n_pass;
     const u64 p = tile * TP + (u64)tid * (V * 4);
     const bool act = p < a.S;
     for (u32 pass = 0; pass < passes; pass++) {
@@ -281,7 +281,9 @@ __global__ void __launch_bounds__(GT * G + 32, G == 1 ? 2 : 1) rlc_kernel(const 
       u32 wn[V], wp[V], pe[V];
 #pragma unroll
       for (int v = 0; v < V; v++) wn[v] = wp[v] = pe[v] = 0u;
-      for (u32 j = 0; j < h.n_terms; j++, q++) {
+      const u32 e1 = sm[h.off_pstart + pass + 1];
+      for (u32 e = sm[h.off_pstart + pass]; e < e1; e++, q++) {
+        const u32 j = sm[h.off_seq + e];
         const u32 k = q / TPS, sub = q - k * TPS, s = k % D;
         if (sub == 0) mbar_wait(bar_full + 8 * s, (k / D) & 1);
         u32 x[V];

@@ -16,11 +16,16 @@ namespace pmrc_rt {
 //   outs[2 r]      = slot,  outs[2 r + 1] = blk
 //   masks[i * n_rb + b] = bit j set iff A[b R + j][i] != 0     (row blocks of R rows)
 //   tabA[4 (i n_out + r)] = (T0a, T0b, T1a, T1b) of A[r][i], tabB[i n_out + r] = T2  (last in the blob)
+//   pstart[p] .. pstart[p + 1]: the pass-p slice of seq; seq[e] = the terms pass p streams (every term
+//     of each input that some row of the pass reads, in input order: a pass skips inputs its G R
+//     rows do not use, e.g. the other symbol groups' inputs of an MBR encode)
 struct RlcHdr {
   uint32_t magic;  // kRlcMagic
   uint32_t words;  // total blob words
   uint32_t n_in, n_out, n_terms, R, n_rb, flags;   // n_rb = ceil(n_out / R) row blocks
   uint32_t off_tabA, off_tabB, off_ttabA, off_ttabB, off_terms, off_outs, off_masks, smem_words;
+  uint32_t G, n_pass, off_pstart, off_seq;         // n_pass = ceil(n_rb / G); seq_len = pstart[n_pass]
+  uint32_t seq_len, pad0, pad1, pad2;
 };
 constexpr uint32_t kRlcGlobalTables = 1u;  // flags: coefficient tables stay in device memory
 constexpr uint32_t kRlcMagic = 0x524C4331u;  // "RLC1"

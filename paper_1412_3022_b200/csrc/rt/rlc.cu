@@ -79,14 +79,17 @@ struct Sel {
 struct Shifts {
   u32 sh3, sh6, sh12;  // 2^29, 2^26, 2^20 (kernel parameters, see RlcArgs)
 };
+// Per word: 3 LOP3 (masks) + 3 LEA.HI (u + (u >> 12): a literal power of two makes ptxas emit
+// one LEA.HI, where a run-time multiplier with an addend costs IMAD.HI + a MOV of the zero half of
+// its 64-bit addend) + 2 IMAD.HI (the plain shifts, run-time multipliers: FMA pipe, RZ addend).
 static __device__ __forceinline__ Sel make_sel(u32 w, const Shifts &k) {
   Sel s;
   const u32 u0 = w & 0x07070707u;
-  s.s0 = madhi(u0, k.sh12, u0);                      // u0 + (u0 >> 12)
+  s.s0 = madhi(u0, 1u << 20, u0);                    // u0 + (u0 >> 12)
   const u32 u1 = madhi(w, k.sh3, 0u) & 0x07070707u;  // (w >> 3) & 7 per byte
-  s.s1 = madhi(u1, k.sh12, u1);
+  s.s1 = madhi(u1, 1u << 20, u1);
   const u32 u2 = madhi(w, k.sh6, 0u) & 0x03030303u;  // (w >> 6) & 3 per byte
-  s.s2 = madhi(u2, k.sh12, u2);
+  s.s2 = madhi(u2, 1u << 20, u2);
   return s;
 }
 // acc ^= c * w (permuted byte order); c's tables t = (T0a, T0b, T1a, T1b), t2 = T2

@@ -254,6 +254,28 @@ def test_encode_host_path_equals_device_path():
         st.close()
 
 
+def test_encode_host_block_size_grows_between_calls():
+    # the host path's staging ring must follow the block size, not only the stripe
+    # count: a small S then a larger S on one handle (same stripes) must stay bit-exact
+    k, n = 8, 16
+    code = pm.pmrc_create(pm.PMRC_MSR_SPARSE, k, 14, n)
+    try:
+        for S, stripes in ((64 * 1024, 1), (1 << 20, 1), (16 * 1024, 3), (2 << 20, 2)):
+            x = inputs.stripe_data(stripes, 56, S, seed=S)
+            hd = torch.from_numpy(x).pin_memory()
+            hp = torch.zeros((stripes, 56, S), dtype=torch.uint8).pin_memory()
+            pm.pmrc_encode_host(code, hd.data_ptr(), hp.data_ptr(), S, stripes, torch.cuda.current_stream().cuda_stream)
+            d = torch.from_numpy(x).to(DEV)
+            par = torch.empty((stripes, 56, S), dtype=torch.uint8, device=DEV)
+            pm.pmrc_encode(code, d.data_ptr(), par.data_ptr(), S, stripes, torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            assert torch.equal(hp, par.cpu()), S
+            w = min(S, 4096)
+            assert np.array_equal(hp[:, :, :w].numpy(), O.encode(O.MSR_SPARSE, n, k, 14, x[:, :, :w]))
+    finally:
+        pm.pmrc_destroy(code)
+
+
 def test_full_size_config2_sampled():
     # config 2 in the bench's launch configuration: 1 GiB real data (R11: 19 stripes of 56 x 1 MiB,
     # last one zero padded), generated on the device; sampled stripes and byte windows vs oracle

@@ -17,6 +17,9 @@ def main():
     op = sys.argv[1]
     kind = int(os.environ.get("KIND", MSR))
     j = Job(kind, 8, 16, int(os.environ.get("S", 1 << 20)))
+    # the generated (JIT) kernels unless PMRC_POLICY=runtime
+    pm.pmrc_set_plan_policy(j.code, pm.PMRC_PLAN_RUNTIME if os.environ.get("PMRC_POLICY") == "runtime"
+                            else pm.PMRC_PLAN_JIT)
     j.encode()
     torch.cuda.synchronize()
     if op == "decode":

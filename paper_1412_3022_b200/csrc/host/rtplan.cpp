@@ -197,6 +197,22 @@ void rt_free(RtPlan &p) {
   p.dev = nullptr;
 }
 
+// estimated ALU work of one tile word of a plan (the batch launches balance CTAs by it): the
+// selectors of every streamed input (per row group), the projections of coefficient terms (per row
+// group), and the row MACs
+double rt_cost(const RtPlan &p) {
+  const uint32_t *b = p.blob.data();
+  const RlcHdr *h = (const RlcHdr *)b;
+  double c = 5.0 * (double)p.nnz;
+  for (uint32_t e = 0; e < h->seq_len; e++) {
+    const uint32_t j = b[h->off_seq + e], w0 = b[h->off_terms + 2 * j];
+    if (!(w0 & 0x80000000u)) c += 8.0 * h->G;  // coefficient term: selectors + product
+    if (w0 & 0x40000000u) c += 8.0 * h->G;     // input complete: its selectors
+    c += 2.0;                                  // staging
+  }
+  return c;
+}
+
 static int sm_count() {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
@@ -252,22 +268,55 @@ int rt_launch(const std::vector<RtPlan *> &plans, const uint16_t *stripe_plan, c
     a.slot_ptr[i] = ptrs[i];
     a.slot_stride[i] = strides[i];
   }
+  const uint64_t TP = (uint64_t)sh.GT * sh.V * 4;
+  const uint64_t tiles = (S + TP - 1) / TP, items = tiles * (uint64_t)stripes;
+  pmrc_rt::RlcShape shx = sh;
+  shx.tg = tg;
+  int per_sm = pmrc_rt::rlc_ctas_per_sm(shx, max_words);
+  if (per_sm < 1) {
+    err = "runtime-coefficient kernel does not fit on an SM (plan too large)";
+    return PMRC_EUNSUPPORTED;
+  }
+  uint64_t grid = (uint64_t)sm_count() * per_sm;
+  if (max_ctas > 0) grid = std::min<uint64_t>(grid, (uint64_t)max_ctas);
+  grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, items));
   void *scratch = nullptr;
   if (stripe_plan) {
-    // per-call launch tables (plan addresses + the stripes' plan indices) in stream-ordered memory
-    const size_t np = plans.size(), bytes = np * 8 + stripes * 2;
-    std::vector<uint8_t> host(bytes);
-    for (size_t i = 0; i < np; i++) {
-      const uint64_t d = (uint64_t)(uintptr_t)plans[i]->dev;
-      memcpy(host.data() + 8 * i, &d, 8);
-    }
+    const size_t np = plans.size();
     for (size_t t = 0; t < stripes; t++) {
       if (stripe_plan[t] >= np && stripe_plan[t] != 0xFFFF) {  // 0xFFFF: nothing to compute in stripe t
         err = "rt_launch: stripe plan index out of range";
         return PMRC_EINVAL;
       }
     }
+    // CTA item ranges of equal estimated cost (ALU work per tile word of each stripe's plan)
+    std::vector<double> pcost(np);
+    for (size_t i = 0; i < np; i++) pcost[i] = rt_cost(*plans[i]);
+    std::vector<uint64_t> bounds(grid + 1, items);
+    double total = 0;
+    for (size_t t = 0; t < stripes; t++) total += stripe_plan[t] == 0xFFFF ? 0.0 : pcost[stripe_plan[t]] * tiles;
+    bounds[0] = 0;
+    {
+      double cum = 0;
+      uint64_t b = 1;
+      for (size_t t = 0; t < stripes && b < grid; t++) {
+        const double c = stripe_plan[t] == 0xFFFF ? 0.0 : pcost[stripe_plan[t]];
+        for (uint64_t j = 0; j < tiles && b < grid; j++) {
+          cum += c;
+          while (b < grid && cum >= total * (double)b / (double)grid) bounds[b++] = t * tiles + j + 1;
+        }
+      }
+    }
+    // per-call launch tables in stream-ordered memory: plan addresses, the stripes' plan indices, the
+    // CTA item bounds
+    const size_t off_b = (np * 8 + stripes * 2 + 7) & ~(size_t)7, bytes = off_b + (grid + 1) * 8;
+    std::vector<uint8_t> host(bytes, 0);
+    for (size_t i = 0; i < np; i++) {
+      const uint64_t d = (uint64_t)(uintptr_t)plans[i]->dev;
+      memcpy(host.data() + 8 * i, &d, 8);
+    }
     memcpy(host.data() + 8 * np, stripe_plan, stripes * 2);
+    memcpy(host.data() + off_b, bounds.data(), (grid + 1) * 8);
     if (cudaMallocAsync(&scratch, bytes, st) != cudaSuccess) {
       cudaGetLastError();
       err = "cudaMallocAsync(launch tables)";
@@ -280,22 +329,10 @@ int rt_launch(const std::vector<RtPlan *> &plans, const uint16_t *stripe_plan, c
     }
     a.plan_ptrs = (const unsigned long long *)scratch;
     a.stripe_plan = (const uint16_t *)((uint8_t *)scratch + 8 * np);
+    a.item_bounds = (const unsigned long long *)((uint8_t *)scratch + off_b);
   } else {
     a.plan0 = (const uint32_t *)plans[0]->dev;
   }
-  const uint64_t TP = (uint64_t)sh.GT * sh.V * 4;
-  const uint64_t items = (S + TP - 1) / TP * (uint64_t)stripes;
-  pmrc_rt::RlcShape shx = sh;
-  shx.tg = tg;
-  int per_sm = pmrc_rt::rlc_ctas_per_sm(shx, max_words);
-  if (per_sm < 1) {
-    err = "runtime-coefficient kernel does not fit on an SM (plan too large)";
-    if (scratch) cudaFreeAsync(scratch, st);
-    return PMRC_EUNSUPPORTED;
-  }
-  uint64_t grid = (uint64_t)sm_count() * per_sm;
-  if (max_ctas > 0) grid = std::min<uint64_t>(grid, (uint64_t)max_ctas);
-  grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, items));
   const int rc = pmrc_rt::rlc_launch(a, shx, (int)grid, stream);
   if (scratch) cudaFreeAsync(scratch, st);
   if (rc) {

@@ -27,6 +27,8 @@ pmrc_rt::RlcShape rt_shape(int n_out, const GenOptions &o);
 // slots, block index >= 65536, tables above kRlcMaxPlanWords).
 int rt_build(const PlanSpec &p, int R, int G, RtPlan &out, std::string &err);
 void rt_free(RtPlan &p);
+// estimated ALU work per tile word (batch launches split CTAs by it)
+double rt_cost(const RtPlan &p);
 
 // Launch: stripe_plan == nullptr -> plans[0] for every stripe; else plans[stripe_plan[t]] (0xFFFF:
 // nothing to compute in stripe t).  All plans must be built for (sh.R, sh.G).  ptrs / strides: n_slots entries

@@ -167,7 +167,10 @@ __global__ void __launch_bounds__(GT * G + 32, G == 1 ? 2 : 1) rlc_kernel(const 
   const u64 items = tiles * a.stripes;
   const u64 per = items / gridDim.x, rem = items % gridDim.x;
   const u64 b = blockIdx.x;
-  const u64 i0 = b * per + (b < rem ? b : rem), i1 = i0 + per + (b < rem ? 1 : 0);
+  // per-stripe patterns of unequal cost (config 4: a parity-node repair costs ~3.6x a systematic
+  // one): the host splits the items by estimated cost; otherwise equal item counts
+  const u64 i0 = a.item_bounds ? a.item_bounds[b] : b * per + (b < rem ? b : rem);
+  const u64 i1 = a.item_bounds ? a.item_bounds[b + 1] : i0 + per + (b < rem ? 1 : 0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < D; s++) {
       mbar_init(bar_full + 8 * s, 1);

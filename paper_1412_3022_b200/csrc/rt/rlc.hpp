@@ -37,6 +37,8 @@ struct RlcArgs {
   const uint32_t *plan0;              // device: the plan of every stripe when stripe_plan == NULL
   const unsigned long long *plan_ptrs; // device: blob address of plan p (batch launches)
   const uint16_t *stripe_plan;        // device: plan index of stripe t, or NULL
+  const unsigned long long *item_bounds;  // device: CTA b walks items [item_bounds[b], item_bounds[b+1]),
+                                          // or NULL (equal item counts per CTA)
   unsigned long long S;               // block bytes (multiple of 16)
   unsigned long long stripes;
   unsigned max_words;                 // largest smem_words of the launch's plans (shared-memory plan area)

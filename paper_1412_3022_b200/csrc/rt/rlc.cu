@@ -304,7 +304,9 @@ __global__ void __launch_bounds__(GT * G + 32, G == 1 ? 2 : 1) rlc_kernel(const 
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_empty + 8 * s);
         }
-        const u32 w0 = sm[h.off_terms + 2 * j];
+        // the term word is the same for the whole warp: broadcast it so the plain / last tests
+        // below compile to uniform branches (no BSSY/BSYNC reconvergence per term)
+        const u32 w0 = __shfl_sync(0xffffffffu, sm[h.off_terms + 2 * j], 0);
         if (w0 & 0x80000000u) {  // plain term (coefficient 1)
 #pragma unroll
           for (int v = 0; v < V; v++) wn[v] ^= x[v];

@@ -45,6 +45,26 @@ def main():
         elif what == "encode":
             par2 = torch.empty_like(par)
             pm.pmrc_encode(code, data.data_ptr(), par2.data_ptr(), S, stripes, st)
+        elif what in ("batch_repair", "batch_decode"):
+            r = inputs.rng(2026)
+            reps, decs = [], []
+            for t in range(stripes):
+                while True:
+                    f = int(r.integers(16))
+                    H = sorted(r.choice([i for i in range(16) if i != f], 14, replace=False).tolist())
+                    om = [i for i in range(16) if i != f and i not in H]
+                    if not (f < a and len(om) == 1 and om[0] < a):
+                        break
+                reps.append((f, H))
+                decs.append(sorted(r.choice(16, 8, replace=False).tolist()))
+            nodes = [piece(i) for i in range(16)]
+            if what == "batch_repair":
+                out = torch.empty((stripes, a, S), dtype=torch.uint8, device="cuda")
+                pm.pmrc_repair_batch(code, [f for f, _ in reps], [H for _, H in reps], nodes, (out.data_ptr(), a * S),
+                                     S, stripes, st)
+            else:
+                dec = torch.zeros_like(data)
+                pm.pmrc_decode_batch(code, decs, nodes, dec.data_ptr(), S, stripes, st)
         elif what == "rs_encode":
             c2, d2, p2, _, _, _, s2, _ = job(pm.PMRC_RS_VANDERMONDE, 8, S)
             pm.pmrc_encode(c2, d2.data_ptr(), p2.data_ptr(), S, s2, st)

@@ -140,6 +140,15 @@ def x_bytes(stripes, B):
     return stripes * B * S_
 
 
+def bench_config(world):
+    """The workload description both arms print (identical dicts: the driver compares them)."""
+    B, P = 56, 56
+    stripes = -(-REAL // (B * S_))
+    return {"workload": WORKLOAD, "S": S_, "stripes_per_gpu": stripes, "real_bytes_per_gpu": REAL,
+            "processed_bytes_per_gpu": stripes * B * S_, "parallelism": "stripes sharded by rank (dp%d)" % world,
+            "l2": "inputs 1 GiB > 126 MB L2 (no flush needed)"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -161,9 +170,9 @@ def run_reference(args):
     out = {"metric": METRIC, "value": v, "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus, "steps": steps,
            "warmup": warmup, "ms_per_step": 1e3 * tot / steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded splitmix64 stream, inputs/)",
-           "config": {"workload": WORKLOAD, "S": S_, "stripes": 19, "sample_per_step": "1 stripe (56 MiB)"},
+           "config": bench_config(int(os.environ.get("WORLD_SIZE", "1"))),
            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                            "sample": "1 stripe (56 MiB of source) per step, plain C oracle, 1 thread"},
+                            "sample": "1 of the 19 stripes (56 MiB of source) per step, plain C oracle, 1 thread"},
            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
     return 0
@@ -341,9 +350,7 @@ def main():
         out = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded splitmix64 uniform bytes, inputs/)",
-               "config": {"workload": WORKLOAD, "S": S_, "stripes_per_gpu": stripes, "real_bytes_per_gpu": REAL,
-                          "processed_bytes_per_gpu": processed, "parallelism": "stripes sharded by rank (dp%d)" % world,
-                          "l2": "inputs 1 GiB > 126 MB L2 (no flush needed)", "init_ms": round(init_s * 1e3, 1)},
+               "config": bench_config(world), "init_ms": round(init_s * 1e3, 1),
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                "clocks": clk.summary(),
                "paper_context": {"value": 0.79, "unit": "GB/s", "what": "1 core Xeon E5-2640, k=8, 16 KB blocks (P:329)"}}

@@ -61,6 +61,7 @@ struct pmrc_code {
   int policy = PMRC_PLAN_AUTO; // engine choice (pmrc_set_plan_policy)
   std::map<std::string, std::unique_ptr<PlanSpec>> specs;  // plan specs by key (null: nothing to compute)
   std::map<std::string, std::unique_ptr<RtPlan>> rt_plans; // runtime-coefficient plans by key + shape
+  bool no_evict = false;       // a batch call holds pointers into the caches: no eviction meanwhile
 };
 
 namespace {
@@ -935,6 +936,9 @@ static bool use_runtime(const pmrc_code *c, const std::string &key) {
   return !c->plans.count(key);
 }
 
+constexpr size_t kMaxRtPlans = 1024;  // runtime plans cached per handle (<= ~160 KB device memory each)
+constexpr size_t kMaxSpecs = 8192;     // plan specs cached per handle
+
 static std::string rt_key(const std::string &key, int R, int G) {
   return key + "#rt" + std::to_string(R) + "x" + std::to_string(G);
 }
@@ -946,6 +950,16 @@ static int get_rt_plan(pmrc_code *c, const std::string &key, const PlanSpec &spe
   if (it != c->rt_plans.end()) {
     *out = it->second.get();
     return PMRC_OK;
+  }
+  if (c->rt_plans.size() >= kMaxRtPlans && !c->no_evict) {
+    // bounded cache (a batch of many patterns per call can add thousands): the device copies may
+    // still be read by launches in flight, so drop them only after the device is idle
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+      cudaGetLastError();
+      return fail(PMRC_ECUDA, "cudaDeviceSynchronize (plan cache eviction)");
+    }
+    for (auto &kv : c->rt_plans) rt_free(*kv.second);
+    c->rt_plans.clear();
   }
   auto p = std::make_unique<RtPlan>();
   std::string err;
@@ -967,6 +981,13 @@ static int get_spec(pmrc_code *c, const std::string &key, Make make, const PlanS
                                                            "Psi_H singular (DESIGN.md R10)"
                                                          : "plan failed (cached)");
   auto it = c->specs.find(key);
+  if (it == c->specs.end() && c->specs.size() >= kMaxSpecs && !c->no_evict) {
+    // bounded host cache of plan specs (only referenced during a call); loaded JIT kernels and
+    // runtime plans keep their own caches
+    c->specs.clear();
+    c->plan_meta.clear();
+    it = c->specs.end();
+  }
   if (it == c->specs.end() || c->dry) {
     auto sp = std::make_unique<PlanSpec>();
     const int rc = make(*sp);
@@ -1331,6 +1352,24 @@ int pmrc_decode_batch(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_
   if (n_surv < 1 || n_surv > D.n) return fail(PMRC_EINVAL, "bad survivor count");
   if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
   if (D.n + 1 > pmrc_rt::kRlcMaxSlots) return fail(PMRC_EUNSUPPORTED, "too many nodes for a batch launch");
+  // the caches are bounded; evict up front, never while this call holds pointers into them
+  if (c->specs.size() + stripes > kMaxSpecs) {
+    c->specs.clear();
+    c->plan_meta.clear();
+  }
+  if (c->rt_plans.size() + stripes > kMaxRtPlans) {
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+      cudaGetLastError();
+      return fail(PMRC_ECUDA, "cudaDeviceSynchronize (plan cache eviction)");
+    }
+    for (auto &kv : c->rt_plans) rt_free(*kv.second);
+    c->rt_plans.clear();
+  }
+  struct NoEvict {
+    pmrc_code *c;
+    ~NoEvict() { c->no_evict = false; }
+  } guard{c};
+  c->no_evict = true;
   std::vector<std::string> keys(stripes);
   std::vector<const PlanSpec *> specs(stripes);
   std::vector<char> used(D.n, 0);
@@ -1366,6 +1405,24 @@ int pmrc_repair_batch(pmrc_code *c, const int *lost_ids, const int *helper_ids, 
   const CodeDef &D = c->def;
   if (S % 16) return fail(PMRC_EALIGN, "S must be a multiple of 16");
   if (D.n + 1 > pmrc_rt::kRlcMaxSlots) return fail(PMRC_EUNSUPPORTED, "too many nodes for a batch launch");
+  // the caches are bounded; evict up front, never while this call holds pointers into them
+  if (c->specs.size() + stripes > kMaxSpecs) {
+    c->specs.clear();
+    c->plan_meta.clear();
+  }
+  if (c->rt_plans.size() + stripes > kMaxRtPlans) {
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+      cudaGetLastError();
+      return fail(PMRC_ECUDA, "cudaDeviceSynchronize (plan cache eviction)");
+    }
+    for (auto &kv : c->rt_plans) rt_free(*kv.second);
+    c->rt_plans.clear();
+  }
+  struct NoEvict {
+    pmrc_code *c;
+    ~NoEvict() { c->no_evict = false; }
+  } guard{c};
+  c->no_evict = true;
   std::vector<std::string> keys(stripes);
   std::vector<const PlanSpec *> specs(stripes);
   std::vector<char> used(D.n, 0);

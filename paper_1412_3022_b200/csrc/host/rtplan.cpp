@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstddef>
 #include <cstring>
 
@@ -194,7 +195,9 @@ int rt_build(const PlanSpec &p, int R, int G, RtPlan &out, std::string &err) {
 
 void rt_free(RtPlan &p) {
   if (p.dev) cudaFree(p.dev);
+  if (p.ready) cudaEventDestroy((cudaEvent_t)p.ready);
   p.dev = nullptr;
+  p.ready = nullptr;
 }
 
 // estimated ALU work of one tile word of a plan (the batch launches balance CTAs by it): the
@@ -248,11 +251,17 @@ int rt_launch(const std::vector<RtPlan *> &plans, const uint16_t *stripe_plan, c
         err = "cudaMalloc(plan)";
         return PMRC_ENOMEM;
       }
-      // the host blob lives in the cached plan, so the async copy's source outlives it
-      if (cudaMemcpyAsync(p->dev, p->blob.data(), nb, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+      // the host blob lives in the cached plan, so the async copy's source outlives it; the event
+      // orders later launches on other streams after the upload
+      if (cudaMemcpyAsync(p->dev, p->blob.data(), nb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+          cudaEventCreateWithFlags((cudaEvent_t *)&p->ready, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventRecord((cudaEvent_t)p->ready, st) != cudaSuccess) {
         err = std::string("plan upload: ") + cudaGetErrorString(cudaGetLastError());
         return PMRC_ECUDA;
       }
+    } else if (p->ready && cudaStreamWaitEvent(st, (cudaEvent_t)p->ready, 0) != cudaSuccess) {
+      err = std::string("plan upload wait: ") + cudaGetErrorString(cudaGetLastError());
+      return PMRC_ECUDA;
     }
   }
   RlcArgs a;
@@ -297,14 +306,20 @@ int rt_launch(const std::vector<RtPlan *> &plans, const uint16_t *stripe_plan, c
     for (size_t t = 0; t < stripes; t++) total += stripe_plan[t] == 0xFFFF ? 0.0 : pcost[stripe_plan[t]] * tiles;
     bounds[0] = 0;
     {
+      // walk the stripes (O(stripes + grid)): boundary b goes after the first item at which the
+      // cumulative cost reaches b / grid of the total; items of one stripe cost the same
       double cum = 0;
       uint64_t b = 1;
       for (size_t t = 0; t < stripes && b < grid; t++) {
         const double c = stripe_plan[t] == 0xFFFF ? 0.0 : pcost[stripe_plan[t]];
-        for (uint64_t j = 0; j < tiles && b < grid; j++) {
-          cum += c;
-          while (b < grid && cum >= total * (double)b / (double)grid) bounds[b++] = t * tiles + j + 1;
+        if (c <= 0.0) continue;
+        while (b < grid) {
+          const double need = total * (double)b / (double)grid - cum;  // cost still missing for b
+          const double jn = std::ceil(need / c - 1e-9);                   // items of stripe t it takes
+          if (jn > (double)tiles) break;
+          bounds[b++] = t * tiles + (uint64_t)std::max(1.0, jn);
         }
+        cum += c * (double)tiles;
       }
     }
     // per-call launch tables in stream-ordered memory: plan addresses, the stripes' plan indices, the

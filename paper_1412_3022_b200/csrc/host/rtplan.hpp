@@ -15,6 +15,7 @@ namespace pmrc {
 struct RtPlan {
   std::vector<uint32_t> blob;  // host copy (rlc.hpp RlcHdr layout)
   void *dev = nullptr;         // device copy (cudaMalloc), uploaded on first launch
+  void *ready = nullptr;       // cudaEvent_t recorded after the upload (other streams wait on it)
   int R = 8, G = 1;            // rows per thread (row-block size of the masks), row groups per pass
   int n_in = 0, n_out = 0, n_terms = 0;
   long nnz = 0;                // nonzero A entries (MACs per 4 byte positions: nnz + derived terms)

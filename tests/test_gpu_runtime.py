@@ -194,3 +194,56 @@ def test_full_size_config4_batch():
                 assert torch.equal(dec[t, miss], data[t, miss]), (t, ids)
     finally:
         pm.pmrc_destroy(code)
+
+
+def test_batch_many_small_stripes_and_empty_calls():
+    # thousands of stripes of one 1 KiB tile each (the CTA item ranges are balanced by each stripe's
+    # plan cost across many plan switches), and the empty calls (no stripes / S = 0) do nothing
+    k, n, S, stripes = 8, 16, 1024, 3000
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=123)
+    try:
+        st.encode()
+        reps, decs = _patterns(pm.PMRC_MSR_SPARSE, k, n, st.d, 40, seed=77)
+        reps = [reps[t % 40] for t in range(stripes)]
+        decs = [decs[t % 40] for t in range(stripes)]
+        out = torch.zeros((stripes, st.alpha, S), dtype=torch.uint8, device=DEV)
+        pm.pmrc_repair_batch(st.code, [f for f, _ in reps], [H for _, H in reps], st.nodes(),
+                             (out.data_ptr(), st.alpha * S), S, stripes, st.stream)
+        dec = torch.zeros_like(st.data)
+        pm.pmrc_decode_batch(st.code, decs, st.nodes(), dec.data_ptr(), S, stripes, st.stream)
+        torch.cuda.synchronize()
+        for t in range(stripes):
+            f = reps[t][0]
+            assert torch.equal(out[t], st.piece_tensor(f)[t]), t
+            miss = _missing(st, decs[t])
+            if miss:
+                assert torch.equal(dec[t, miss], st.data[t, miss]), t
+        before = out.clone()
+        pm.pmrc_repair_batch(st.code, [], [], st.nodes(), (out.data_ptr(), st.alpha * S), S, 0, st.stream)
+        pm.pmrc_repair_batch(st.code, [f for f, _ in reps], [H for _, H in reps], st.nodes(),
+                             (out.data_ptr(), st.alpha * S), 0, stripes, st.stream)
+        torch.cuda.synchronize()
+        assert torch.equal(before, out)
+    finally:
+        st.close()
+
+
+def test_new_plan_used_on_another_stream_right_away():
+    # a runtime plan uploaded on stream A (its first call) and used by a launch on stream B issued
+    # immediately after: the launch waits for the upload (event), so the result is exact
+    k, n, S, stripes = 8, 16, 256 * 1024, 3
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=321, policy=pm.PMRC_PLAN_RUNTIME)
+    try:
+        st.encode()
+        a_, b_ = torch.cuda.Stream(), torch.cuda.Stream()
+        ids = [2, 3, 6, 7, 8, 10, 11, 13]
+        outs = [torch.zeros_like(st.data) for _ in range(2)]
+        torch.cuda.synchronize()
+        pm.pmrc_decode(st.code, ids, [st.piece(i) for i in ids], outs[0].data_ptr(), S, stripes, a_.cuda_stream)
+        pm.pmrc_decode(st.code, ids, [st.piece(i) for i in ids], outs[1].data_ptr(), S, stripes, b_.cuda_stream)
+        torch.cuda.synchronize()
+        miss = _missing(st, ids)
+        for o in outs:
+            assert torch.equal(o[:, miss], st.data[:, miss])
+    finally:
+        st.close()

@@ -20,11 +20,13 @@ pmrc_rt::RlcShape rt_shape(int n_out, const GenOptions &o) {
   // R rows x V words of accumulators per thread, G row groups of GT threads per CTA (a pass covers
   // G R rows; measured, profiles/r02):
   //   <= 8 rows (repair, projections, RS encode): (8, 4, 1, 256), two CTAs per SM
-  //   more (decode, encode): (8, 4, 2, 256), 16 rows per pass (shapes with V = 2 and more groups
-  //   measured slower: twice the per-word instruction overhead)
+  //   more (decode, encode): (8, 4, 2, 256), 16 rows per pass (measured against it and slower:
+  //   V = 2 with 3 or 7 groups -- twice the per-word overhead; 16 rows x 2 words in one group,
+  //   which saves the second group's selectors: config-4 decode 2.58 -> 2.85 ms, repair 0.94 -> 1.37)
   // (rt_groups overrides for experiments; tg is set per launch from the plans)
   pmrc_rt::RlcShape sh = n_out <= 8 ? pmrc_rt::RlcShape{8, 4, 1, 256, false} : pmrc_rt::RlcShape{8, 4, 2, 256, false};
-  if (o.rt_groups == 1 || o.rt_groups == 2) sh.G = o.rt_groups;
+  if (o.rt_groups == 1) sh = {8, 4, 1, 256, false};
+  if (o.rt_groups == 2) sh = {8, 4, 2, 256, false};
   return sh;
 }
 

@@ -338,17 +338,21 @@ __global__ void __launch_bounds__(GT * G + 32, G == 1 ? 2 : 1) rlc_kernel(const 
           // this is the common case): no branches, all R rows' tables loaded up front, and the
           // R x V independent MAC chains interleave freely (rows past n_out of a short last block
           // compute garbage that is never stored)
-          uint4 tb[R];
-          u32 t2[R];
+          constexpr int RB = R < 8 ? R : 8;  // tables loaded 8 rows at a time (registers)
 #pragma unroll
-          for (int r = 0; r < R; r++) {
-            tb[r] = *(const uint4 *)(tA + 4 * r);
-            t2[r] = tB[r];
+          for (int r0 = 0; r0 < R; r0 += RB) {
+            uint4 tb[RB];
+            u32 t2[RB];
+#pragma unroll
+            for (int r = 0; r < RB; r++) {
+              tb[r] = *(const uint4 *)(tA + 4 * (r0 + r));
+              t2[r] = tB[r0 + r];
+            }
+#pragma unroll
+            for (int r = 0; r < RB; r++)
+#pragma unroll
+              for (int v = 0; v < V; v++) mac(acc[r0 + r][v], tb[r], t2[r], sl[v]);
           }
-#pragma unroll
-          for (int r = 0; r < R; r++)
-#pragma unroll
-            for (int v = 0; v < V; v++) mac(acc[r][v], tb[r], t2[r], sl[v]);
           continue;
         }
         uint4 tbn = *(const uint4 *)tA;

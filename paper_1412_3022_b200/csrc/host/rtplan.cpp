@@ -342,6 +342,7 @@ int rt_launch(const std::vector<RtPlan *> &plans, const uint16_t *stripe_plan, c
     // pageable source: staged before cudaMemcpyAsync returns, so `host` may go out of scope
     if (cudaMemcpyAsync(scratch, host.data(), bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) {
       err = std::string("launch tables: ") + cudaGetErrorString(cudaGetLastError());
+      cudaFreeAsync(scratch, st);
       return PMRC_ECUDA;
     }
     a.plan_ptrs = (const unsigned long long *)scratch;

@@ -175,6 +175,13 @@ int pmrc_get_plan_policy(const pmrc_code *c);
  * pmrc_decode / pmrc_repair. */
 int pmrc_plan_prepare(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids);
 
+/* The runtime-coefficient kernel's plan blob (u32 words; layout: csrc/rt/rlc.hpp RlcHdr) of a decode
+ * (op 0, ids = survivors), repair (op 1, lost_id, ids = helpers) or encode (op 2) plan, built on the
+ * host without a GPU (slots: survivor / helper index in ascending id order, then the output).
+ * *n_words receives the length; buf (may be NULL) receives the words when cap >= *n_words. */
+int pmrc_rt_plan_blob(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids, uint32_t *buf, size_t cap,
+                      size_t *n_words);
+
 /* Per-stripe failure patterns in ONE launch (config 4 as BASELINE.json states it; the
  * initialisation "depends on the failure pattern but can be reused across stripes"): stripe t has
  * its own pattern, run by the runtime-coefficient kernel (GF(2^8) codes).  nodes[i] (i < n) is node

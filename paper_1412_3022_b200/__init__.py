@@ -25,7 +25,8 @@ EXPORTS = ["pmrc_create", "pmrc_destroy", "pmrc_info", "pmrc_matrix", "pmrc_layo
            "pmrc_read_cost", "pmrc_launch_count", "pmrc_strerror", "pmrc_last_error", "pmrc_precompile",
            "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source", "pmrc_plan_stats", "pmrc_apply", "pmrc_apply_stats", "pmrc_set_max_ctas",
            "pmrc_set_independent_launches", "pmrc_set_plan_policy", "pmrc_get_plan_policy", "pmrc_plan_prepare",
-           "pmrc_decode_batch", "pmrc_repair_batch", "pmrc_decode_specific", "pmrc_decode_specific_scratch"]
+           "pmrc_decode_batch", "pmrc_repair_batch", "pmrc_decode_specific", "pmrc_decode_specific_scratch",
+           "pmrc_rt_plan_blob"]
 
 
 class PmrcError(RuntimeError):
@@ -99,6 +100,7 @@ def lib():
             "pmrc_repair_batch": ([P, IP, IP, I, ctypes.POINTER(pmrc_cregion), pmrc_region, Z, Z, P], I),
             "pmrc_decode_specific_scratch": ([P, Z, Z, ctypes.POINTER(ctypes.c_size_t)], I),
             "pmrc_decode_specific": ([P, IP, I, ctypes.POINTER(pmrc_cregion), P, P, Z, Z, Z, IP, P], I),
+            "pmrc_rt_plan_blob": ([P, I, I, IP, I, P, Z, ctypes.POINTER(ctypes.c_size_t)], I),
             "pmrc_strerror": ([I], ctypes.c_char_p),
             "pmrc_last_error": ([], ctypes.c_char_p),
         }
@@ -303,6 +305,18 @@ def pmrc_decode_specific(code, surv_ids, pieces, data_out_ptr, scratch_ptr, scra
     _check(lib().pmrc_decode_specific(code, ids, n, regs, data_out_ptr, scratch_ptr, scratch_bytes, S, stripes,
                                       ctypes.byref(nw), stream), "pmrc_decode_specific")
     return nw.value
+
+
+def pmrc_rt_plan_blob(code, op, lost_id=0, ids=()):
+    """The runtime-coefficient plan blob (numpy uint32) of a decode (0) / repair (1) / encode (2) plan."""
+    import numpy as np
+    arr, n = _ints(ids)
+    nw = ctypes.c_size_t()
+    _check(lib().pmrc_rt_plan_blob(code, op, lost_id, arr, n, None, 0, ctypes.byref(nw)), "pmrc_rt_plan_blob")
+    out = np.zeros(nw.value, np.uint32)
+    _check(lib().pmrc_rt_plan_blob(code, op, lost_id, arr, n, out.ctypes.data, nw.value, ctypes.byref(nw)),
+           "pmrc_rt_plan_blob")
+    return out
 
 
 def pmrc_apply_stats(code, A):

@@ -1750,6 +1750,45 @@ int pmrc_decode_specific(pmrc_code *c, const int *surv_ids_in, int n_surv, const
   return PMRC_OK;
 }
 
+int pmrc_rt_plan_blob(pmrc_code *c, int op, int lost_id, const int *ids_in, int n_ids, uint32_t *buf, size_t cap,
+                      size_t *n_words) {
+  // the runtime-coefficient kernel's plan blob for a pattern, built on the host (no GPU): for
+  // inspection and for the CPU tier's emulation of the kernel (tests/test_rt_plan.py)
+  if (!c || !n_words) return fail(PMRC_EINVAL, "NULL argument");
+  *n_words = 0;
+  if (c->w != 8) return fail(PMRC_EUNSUPPORTED, "runtime-coefficient plans are GF(2^8) only");
+  const CodeDef &D = c->def;
+  PlanSpec spec;
+  int rc = PMRC_OK;
+  if (op == 2) {
+    spec = c->enc_spec;
+  } else if (op == 0 || op == 1) {
+    if (!ids_in || n_ids < 1 || n_ids > D.n || check_ids(D, ids_in, n_ids)) return fail(PMRC_EINVAL, "bad ids");
+    std::vector<int> ids(ids_in, ids_in + n_ids), slot_of(n_ids);
+    std::sort(ids.begin(), ids.end());
+    for (int q = 0; q < n_ids; q++) slot_of[q] = q;
+    if (op == 0) {
+      rc = decode_spec(c, ids.data(), n_ids, slot_of.data(), n_ids, n_ids + 1, spec);
+      if (rc == kNothing) return fail(PMRC_EINVAL, "no data block is missing (nothing to compute)");
+    } else {
+      int need = 0;
+      rc = repair_common(c, lost_id, ids.data(), n_ids, &need);
+      if (!rc) rc = repair_spec(c, lost_id, ids.data(), n_ids, slot_of.data(), n_ids, n_ids + 1, spec);
+    }
+    if (rc) return rc == PMRC_ESINGULAR ? fail(rc, "singular pattern") : rc;
+  } else {
+    return fail(PMRC_EINVAL, "op must be 0 (decode), 1 (repair) or 2 (encode)");
+  }
+  const pmrc_rt::RlcShape sh = rt_shape((int)spec.outputs.size(), c->gen);
+  RtPlan P;
+  std::string err;
+  rc = rt_build(spec, sh.R, sh.G, P, err);
+  if (rc) return fail(rc, err);
+  *n_words = P.blob.size();
+  if (buf && cap >= P.blob.size()) memcpy(buf, P.blob.data(), P.blob.size() * 4);
+  return PMRC_OK;
+}
+
 int pmrc_plan_prepare(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids) {
   // promote a (hot) failure pattern to its generated bitsliced kernel: build + NVRTC-compile (or
   // load from the kernel cache) now, so later calls with this pattern run the JIT kernel under

@@ -113,8 +113,10 @@ def test_decode_k8_random_subsets(kind, policy):
     try:
         st.encode()
         r = inputs.rng(4)
-        for _ in range(6):
+        for trial in range(6):
             ids = sorted(r.choice(n, k, replace=False).tolist())
+            if policy == pm.PMRC_PLAN_JIT and trial % 2:
+                continue   # half the sets on the JIT engine (an NVRTC compile each)
             out = st.data.clone()
             lost = [i for i in range(k) if i not in ids]
             # poison the lost systematic blocks, decode in place

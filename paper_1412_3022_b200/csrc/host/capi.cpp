@@ -1027,7 +1027,8 @@ static int run_plan(pmrc_code *c, const std::string &key, const PlanSpec &spec, 
       return PMRC_OK;
     }
     if (!(rc == PMRC_EUNSUPPORTED && c->policy == PMRC_PLAN_AUTO)) return rc;
-    // AUTO: plans the runtime kernel cannot hold (tables above its shared-memory budget) use JIT
+    // AUTO: plans the runtime kernel cannot hold (wiring and masks above its shared-memory budget,
+    // more than kRlcMaxSlots regions) use JIT
   }
   Kernel *K = nullptr;
   int rc = get_kernel(c, key, spec, &K);

@@ -9,9 +9,9 @@
            formulation choice: PRMT tables vs bitsliced XOR networks)
 
 Roofline per measurement: algorithmic HBM bytes (distinct blocks read + written) at the measured
-HBM peak, and the runtime kernel's own ALU issue count (3 PRMT + 2 LOP3 per nonzero coefficient
-per 4 bytes + 3 LOP3 per input word for the selectors) at 148 x 64 lanes/clk x 1.965 GHz, next to
-the SURVEY §8(d) naive-W issue term of the same plan.
+HBM peak; the PRMT formulation's own ALU-pipe work (rt_alu_per_word, counted from the plan blob)
+at 148 x 64 lanes/clk x 1.965 GHz ("rt_formulation_alu_frac" / "rt_alu_frac"); and the SURVEY §8(d)
+naive-W issue term of the same plan ("naive_W_alu_frac").
 """
 import json
 import os
@@ -85,10 +85,33 @@ class Job:
         return self.par[:, (i - self.k) * a:(i - self.k + 1) * a] if i >= self.k else self.data[:, i * a:(i + 1) * a]
 
 
-def rt_ops(code, op, lost, ids, S):
-    """ALU lane-ops per stripe of the runtime kernel for a plan (from its coefficient counts)."""
-    st = pm.pmrc_plan_stats(code, op, lost, ids)
-    return st
+HDR = ["magic", "words", "n_in", "n_out", "n_terms", "R", "n_rb", "flags", "off_tabA", "off_tabB", "off_ttabA",
+       "off_ttabB", "off_terms", "off_outs", "off_masks", "smem_words", "G", "n_pass", "off_pstart", "off_seq",
+       "seq_len"]
+
+
+def rt_alu_per_word(blob):
+    """ALU-pipe lane-ops per 32-bit word position of the runtime kernel's formulation for a plan blob
+    (rlc.cu): every streamed coefficient term 3 LOP3 + 3 LEA.HI (selectors) + 3 PRMT + 1.5 LOP3,
+    every completed input 3 + 3 (selectors) + 1 (unpermute), every nonzero coefficient of a row block
+    3 PRMT + 2 LOP3, each counted once per row group that streams it."""
+    h = dict(zip(HDR, [int(v) for v in blob[:len(HDR)]]))
+    ops = 0.0
+    for ps in range(h["n_pass"]):
+        e0, e1 = int(blob[h["off_pstart"] + ps]), int(blob[h["off_pstart"] + ps + 1])
+        for g in range(h["G"]):
+            rb = ps * h["G"] + g
+            if rb >= h["n_rb"]:
+                continue
+            for e in range(e0, e1):
+                j = int(blob[h["off_seq"] + e])
+                w0, w1 = int(blob[h["off_terms"] + 2 * j]), int(blob[h["off_terms"] + 2 * j + 1])
+                if not w0 & 0x80000000:
+                    ops += 10.5
+                if w0 & 0x40000000:
+                    mask = int(blob[h["off_masks"] + (w1 >> 16) * h["n_rb"] + rb])
+                    ops += 7 + 5 * bin(mask).count("1")
+    return ops
 
 
 def config4_batch(steps):
@@ -128,29 +151,27 @@ def config4_batch(steps):
     # algorithmic bytes: repair reads nnz(mu) blocks per helper, writes alpha; decode reads the used
     # survivor blocks, writes the missing data blocks (pmrc_plan_stats per pattern)
     rb = db = 0
-    r_ops = d_ops = 0
+    r_ops = d_ops = 0.0
     for f, H in reps:
         s = pm.pmrc_plan_stats(j.code, 1, f, H)
         rb += (s["in_blocks"] + s["out_blocks"]) * S
-        mu = pm.pmrc_read_cost(j.code, f)
-        # runtime ALU ops per 4 positions: terms with mu != 1 -> 5 + 3 (selectors); rows: 5 per nnz + 3 per input
-        r_ops += (len(H) * (mu * (5 if mu > 1 else 0) + 3 * (mu > 1)) + 5 * a * len(H) + 3 * len(H)) * (S // 4)
+        r_ops += rt_alu_per_word(pm.pmrc_rt_plan_blob(j.code, 1, f, H)) * (S // 4)
     for ids in decs:
         try:
             s = pm.pmrc_plan_stats(j.code, 0, 0, ids)
         except pm.PmrcError:
             continue
         db += (s["in_blocks"] + s["out_blocks"]) * S
-        d_ops += (5 * s["out_blocks"] * s["in_blocks"] + 3 * s["in_blocks"]) * (S // 4)   # dense upper bound
+        d_ops += rt_alu_per_word(pm.pmrc_rt_plan_blob(j.code, 0, 0, ids)) * (S // 4)
     hb = hbm_peak()
     emit({"op": "repair_batch", "config": "config4", "stripes": j.stripes, "launches": 1, "bit_exact": ok_r,
           "singular_rejected": rej, "ms": round(ms_r, 4), "GBps_repaired": round(j.stripes * a * S / ms_r / 1e6, 1),
           "host_init_ms": round(init_r * 1e3, 2), "hbm_bytes": rb, "hbm_frac": round(rb / hb / (ms_r * 1e-3), 3),
-          "rt_alu_frac_upper": round(r_ops / ALU / (ms_r * 1e-3), 3)})
+          "rt_alu_frac": round(r_ops / ALU / (ms_r * 1e-3), 3)})
     emit({"op": "decode_batch", "config": "config4", "stripes": j.stripes, "launches": 1, "bit_exact": ok_d,
           "ms": round(ms_d, 4), "GBps": round(j.stripes * j.B * S / ms_d / 1e6, 1),
           "host_init_ms": round(init_d * 1e3, 2), "hbm_bytes": db, "hbm_frac": round(db / hb / (ms_d * 1e-3), 3),
-          "rt_alu_frac_dense_bound": round(d_ops / ALU / (ms_d * 1e-3), 3)})
+          "rt_alu_frac": round(d_ops / ALU / (ms_d * 1e-3), 3)})
     return j
 
 
@@ -173,9 +194,11 @@ def single(j, steps):
             ms = timed(fn, steps)
             s = pm.pmrc_plan_stats(j.code, 1, f, H)
             byts = (s["in_blocks"] + s["out_blocks"]) * S * j.stripes
+            rt = rt_alu_per_word(pm.pmrc_rt_plan_blob(j.code, 1, f, H)) * (S // 4) * j.stripes
             emit({"op": "repair", "engine": name, "lost": f, "bit_exact": ok, "ms": round(ms, 4),
                   "GBps_repaired": round(j.stripes * a * S / ms / 1e6, 1), "first_call_s": round(init, 3),
-                  "hbm_frac": round(byts / hbm_peak() / (ms * 1e-3), 3)})
+                  "hbm_frac": round(byts / hbm_peak() / (ms * 1e-3), 3),
+                  "rt_formulation_alu_frac": round(rt / ALU / (ms * 1e-3), 3)})
         dec = torch.zeros_like(j.data)
         fn = lambda: pm.pmrc_decode(j.code, ids, [j.piece(i) for i in ids], dec.data_ptr(), S, j.stripes, j.st)
         t0 = time.perf_counter()
@@ -188,10 +211,12 @@ def single(j, steps):
         s = pm.pmrc_plan_stats(j.code, 0, 0, ids)
         byts = (s["in_blocks"] + s["out_blocks"]) * S * j.stripes
         naive = s["naive_lop3"] * (S // 32) * j.stripes
+        rt = rt_alu_per_word(pm.pmrc_rt_plan_blob(j.code, 0, 0, ids)) * (S // 4) * j.stripes
         emit({"op": "decode", "engine": name, "survivors": ids, "bit_exact": ok, "ms": round(ms, 4),
               "GBps": round(j.stripes * j.B * S / ms / 1e6, 1), "first_call_s": round(init, 3),
               "hbm_frac": round(byts / hbm_peak() / (ms * 1e-3), 3),
-              "naive_W_alu_frac": round(naive / ALU / (ms * 1e-3), 3)})
+              "naive_W_alu_frac": round(naive / ALU / (ms * 1e-3), 3),
+              "rt_formulation_alu_frac": round(rt / ALU / (ms * 1e-3), 3)})
     pm.pmrc_set_plan_policy(j.code, pm.PMRC_PLAN_AUTO)
 
 
@@ -210,7 +235,7 @@ def encode_cmp(steps):
             info = pm.pmrc_info(j.code)
             naive = info["xor_ops_naive"] * (S // 32) * j.stripes
             byts = (j.B + j.P) * S * j.stripes
-            rt = (5 * info["nnz"] + 3 * j.B) * (S // 4) * j.stripes
+            rt = rt_alu_per_word(pm.pmrc_rt_plan_blob(j.code, 2)) * (S // 4) * j.stripes
             emit({"op": "encode", "engine": name, "kind": kind, "k": k, "S": S, "same_as_jit": ok, "ms": round(ms, 4),
                   "GBps": round(j.stripes * j.B * S / ms / 1e6, 1),
                   "naive_W_alu_frac": round(naive / ALU / (ms * 1e-3), 3),

@@ -141,3 +141,26 @@ def test_rt_decode_and_repair_blobs_emulated(kind, k, n):
             assert np.array_equal(out, piece(f)), (f, H)
     finally:
         pm.pmrc_destroy(code)
+
+
+def test_rt_decode_blob_k16_tables_in_device_memory():
+    # k = 16 decode from 16 parity nodes: 240 x 240 coefficients (1.15 MB of tables) exceed the
+    # shared-memory budget, so the blob flags its tables to be read from device memory; the
+    # emulation of that blob still returns the data
+    kind, k, n, d = 0, 16, 32, 30
+    code = pm.pmrc_create(kind, k, d, n)
+    try:
+        info = pm.pmrc_info(code)
+        B, a = info["B"], info["alpha"]
+        S = 16
+        x = inputs.stripe_data(1, B, S, seed=161)[0]
+        par = O.encode(O.MSR_SPARSE, n, k, d, x[None])[0]
+        ids = list(range(16, 32))
+        blob = pm.pmrc_rt_plan_blob(code, 0, 0, ids)
+        h = dict(zip(HDR, [int(v) for v in blob[:len(HDR)]]))
+        assert h["flags"] & 1 and h["smem_words"] == h["off_tabA"] < h["words"]
+        out = np.zeros((B, S), np.uint8)
+        emulate(blob, {q: par[(i - k) * a:(i - k + 1) * a] for q, i in enumerate(ids)}, {len(ids): out})
+        assert np.array_equal(out, x)
+    finally:
+        pm.pmrc_destroy(code)

@@ -157,9 +157,11 @@ int rt_build(const PlanSpec &p, int R, int G, RtPlan &out, std::string &err) {
   std::copy(masks.begin(), masks.end(), b.begin() + h.off_masks);
   std::copy(pstart.begin(), pstart.end(), b.begin() + h.off_pstart);
   std::copy(seq.begin(), seq.end(), b.begin() + h.off_seq);
-  int q = 0;
+  int q = 0, n_plain = 0;
+  bool single = true;  // every input is one term
   for (int i = 0; i < n_in; i++) {
     const auto &terms = p.inputs[i].terms;
+    single &= terms.size() == 1;
     for (size_t j = 0; j < terms.size(); j++, q++) {
       const Term &t = terms[j];
       if (t.slot < 0 || t.slot >= p.n_slots || t.blk < 0 || t.blk > 65535 || t.coef == 0 || t.coef > 255) {
@@ -168,12 +170,17 @@ int rt_build(const PlanSpec &p, int R, int G, RtPlan &out, std::string &err) {
       }
       uint32_t w0 = (uint32_t)t.slot;
       if (j + 1 == terms.size()) w0 |= 0x40000000u;
-      if (t.coef == 1) w0 |= 0x80000000u;
-      else tables((uint8_t)t.coef, &b[h.off_ttabA + 4 * q], &b[h.off_ttabB + q]);
+      if (t.coef == 1) {
+        w0 |= 0x80000000u;
+        n_plain++;
+      } else tables((uint8_t)t.coef, &b[h.off_ttabA + 4 * q], &b[h.off_ttabB + q]);
       b[h.off_terms + 2 * q] = w0;
       b[h.off_terms + 2 * q + 1] = (uint32_t)t.blk | ((uint32_t)i << 16);
     }
   }
+  // the kernel's loop for this term structure (rlc.cu)
+  if (single && n_plain == n_terms) h.flags |= pmrc_rt::kRlcDirect;
+  if (n_plain == 0) h.flags |= pmrc_rt::kRlcNoPlain;
   for (int r = 0; r < n_out; r++) {
     const OutputDesc &o = p.outputs[ord[r]];
     if (o.slot < 0 || o.slot >= p.n_slots || o.blk < 0) {

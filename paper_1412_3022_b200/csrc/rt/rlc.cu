@@ -284,15 +284,11 @@ __global__ void __launch_bounds__(GT * G + 32, G == 1 ? 2 : 1) rlc_kernel(const 
       for (int r = 0; r < R; r++)
 #pragma unroll
         for (int v = 0; v < V; v++) acc[r][v] = 0u;
-      u32 wn[V], wp[V], pe[V];
-#pragma unroll
-      for (int v = 0; v < V; v++) wn[v] = wp[v] = pe[v] = 0u;
-      const u32 e1 = sm[h.off_pstart + pass + 1];
-      for (u32 e = sm[h.off_pstart + pass]; e < e1; e++, q++) {
+      // the term stream of this pass: slot wait, this thread's words, slot release
+      auto fetch = [&](u32 e, u32 (&x)[V]) -> u32 {
         const u32 j = sm[h.off_seq + e];
         const u32 k = q / TPS, sub = q - k * TPS, s = k % D;
         if (sub == 0) mbar_wait(bar_full + 8 * s, (k / D) & 1);
-        u32 x[V];
         if (V == 4) {
           const uint4 v4 = *(const uint4 *)(ring + s * SLOT + sub * TP + tid * 16);
           x[0] = v4.x; x[1 % V] = v4.y; x[2 % V] = v4.z; x[3 % V] = v4.w;
@@ -304,33 +300,15 @@ __global__ void __launch_bounds__(GT * G + 32, G == 1 ? 2 : 1) rlc_kernel(const 
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_empty + 8 * s);
         }
-        // the term word is the same for the whole warp: broadcast it so the plain / last tests
-        // below compile to uniform branches (no BSSY/BSYNC reconvergence per term)
-        const u32 w0 = __shfl_sync(0xffffffffu, sm[h.off_terms + 2 * j], 0);
-        if (w0 & 0x80000000u) {  // plain term (coefficient 1)
-#pragma unroll
-          for (int v = 0; v < V; v++) wn[v] ^= x[v];
-        } else {
-          const uint4 tb = *(const uint4 *)(sm + h.off_ttabA + 4 * j);
-          const u32 t2 = sm[h.off_ttabB + j];
-#pragma unroll
-          for (int v = 0; v < V; v++) mac_pend(wp[v], pe[v], tb, t2, make_sel(x[v], ks));
-        }
-        if (!(w0 & 0x40000000u)) continue;  // more terms of this input follow
-        // the input is complete: apply it to this group's rows
-        const u32 i = sm[h.off_terms + 2 * j + 1] >> 16;
+        return j;
+      };
+      // a complete (derived) input i, natural byte order: apply it to this group's rows
+      auto apply = [&](u32 i, const u32 (&win)[V]) {
         const u32 mask = __shfl_sync(0xffffffffu, rows_here ? sm[h.off_masks + i * n_rb + rb] : 0u, 0);
-        if (!mask) {
-#pragma unroll
-          for (int v = 0; v < V; v++) wn[v] = wp[v] = pe[v] = 0u;
-          continue;
-        }
+        if (!mask) return;
         Sel sl[V];
 #pragma unroll
-        for (int v = 0; v < V; v++) {
-          sl[v] = make_sel(wn[v] ^ unperm(wp[v] ^ pe[v]), ks);
-          wn[v] = wp[v] = pe[v] = 0u;
-        }
+        for (int v = 0; v < V; v++) sl[v] = make_sel(win[v], ks);
         const u32 *tA = tabs + h.off_tabA + 4 * (i * h.n_out + rb * R);
         const u32 *tB = tabs + h.off_tabB + i * h.n_out + rb * R;
         if (mask == vmask) {
@@ -353,7 +331,7 @@ __global__ void __launch_bounds__(GT * G + 32, G == 1 ? 2 : 1) rlc_kernel(const 
 #pragma unroll
               for (int v = 0; v < V; v++) mac(acc[r0 + r][v], tb[r], t2[r], sl[v]);
           }
-          continue;
+          return;
         }
         uint4 tbn = *(const uint4 *)tA;
         u32 t2n = tB[0];
@@ -369,6 +347,68 @@ __global__ void __launch_bounds__(GT * G + 32, G == 1 ? 2 : 1) rlc_kernel(const 
 #pragma unroll
             for (int v = 0; v < V; v++) mac(acc[r][v], tb, t2, sl[v]);
           }
+        }
+      };
+      const u32 e0 = sm[h.off_pstart + pass], e1 = sm[h.off_pstart + pass + 1];
+      // the plan's term structure (uniform per plan) picks one of three loops, so that no loop
+      // carries state it does not need (a mixed loop's branch joins cost register moves)
+      const u32 mode = h.flags & (kRlcDirect | kRlcNoPlain);
+      if (mode == kRlcDirect) {
+        // every input is one plain term (encode, decode, systematic repair)
+        for (u32 e = e0; e < e1; e++, q++) {
+          u32 x[V];
+          const u32 j = fetch(e, x);
+          apply(sm[h.off_terms + 2 * j + 1] >> 16, x);
+        }
+      } else if (mode == kRlcNoPlain) {
+        // every term carries a coefficient (parity-node repair: the helpers' projections)
+        u32 wp[V], pe[V];
+#pragma unroll
+        for (int v = 0; v < V; v++) wp[v] = pe[v] = 0u;
+        for (u32 e = e0; e < e1; e++, q++) {
+          u32 x[V];
+          const u32 j = fetch(e, x);
+          const uint4 tb = *(const uint4 *)(sm + h.off_ttabA + 4 * j);
+          const u32 t2 = sm[h.off_ttabB + j];
+#pragma unroll
+          for (int v = 0; v < V; v++) mac_pend(wp[v], pe[v], tb, t2, make_sel(x[v], ks));
+          const u32 w0 = __shfl_sync(0xffffffffu, sm[h.off_terms + 2 * j], 0);
+          if (!(w0 & 0x40000000u)) continue;  // more terms of this input follow
+          u32 win[V];
+#pragma unroll
+          for (int v = 0; v < V; v++) {
+            win[v] = unperm(wp[v] ^ pe[v]);
+            wp[v] = pe[v] = 0u;
+          }
+          apply(sm[h.off_terms + 2 * j + 1] >> 16, win);
+        }
+      } else {
+        u32 wn[V], wp[V], pe[V];
+#pragma unroll
+        for (int v = 0; v < V; v++) wn[v] = wp[v] = pe[v] = 0u;
+        for (u32 e = e0; e < e1; e++, q++) {
+          u32 x[V];
+          const u32 j = fetch(e, x);
+          // the term word is the same for the whole warp: broadcast it so the plain / last tests
+          // below compile to uniform branches (no BSSY/BSYNC reconvergence per term)
+          const u32 w0 = __shfl_sync(0xffffffffu, sm[h.off_terms + 2 * j], 0);
+          if (w0 & 0x80000000u) {  // plain term (coefficient 1)
+#pragma unroll
+            for (int v = 0; v < V; v++) wn[v] ^= x[v];
+          } else {
+            const uint4 tb = *(const uint4 *)(sm + h.off_ttabA + 4 * j);
+            const u32 t2 = sm[h.off_ttabB + j];
+#pragma unroll
+            for (int v = 0; v < V; v++) mac_pend(wp[v], pe[v], tb, t2, make_sel(x[v], ks));
+          }
+          if (!(w0 & 0x40000000u)) continue;  // more terms of this input follow
+          u32 win[V];
+#pragma unroll
+          for (int v = 0; v < V; v++) {
+            win[v] = wn[v] ^ unperm(wp[v] ^ pe[v]);
+            wn[v] = wp[v] = pe[v] = 0u;
+          }
+          apply(sm[h.off_terms + 2 * j + 1] >> 16, win);
         }
       }
       if (act && rows_here) {

@@ -28,6 +28,8 @@ struct RlcHdr {
   uint32_t seq_len, pad0, pad1, pad2;
 };
 constexpr uint32_t kRlcGlobalTables = 1u;  // flags: coefficient tables stay in device memory
+constexpr uint32_t kRlcDirect = 2u;        // flags: every input is one plain term (no derived inputs)
+constexpr uint32_t kRlcNoPlain = 4u;       // flags: no term has coefficient 1
 constexpr uint32_t kRlcMagic = 0x524C4331u;  // "RLC1"
 constexpr int kRlcMaxPlanWords = 40 * 1024;  // shared-memory plan budget (160 KB); larger tables stay global
 

@@ -262,7 +262,8 @@ def test_encode_host_block_size_grows_between_calls():
     k, n = 8, 16
     code = pm.pmrc_create(pm.PMRC_MSR_SPARSE, k, 14, n)
     try:
-        for S, stripes in ((64 * 1024, 1), (1 << 20, 1), (16 * 1024, 3), (2 << 20, 2)):
+        # stripes of > 16 MiB go through the host path in column ranges (2-D copies), ragged last one
+        for S, stripes in ((64 * 1024, 1), (1 << 20, 1), (16 * 1024, 3), (2 << 20, 2), ((1 << 20) + 48, 3)):
             x = inputs.stripe_data(stripes, 56, S, seed=S)
             hd = torch.from_numpy(x).pin_memory()
             hp = torch.zeros((stripes, 56, S), dtype=torch.uint8).pin_memory()
@@ -274,6 +275,7 @@ def test_encode_host_block_size_grows_between_calls():
             assert torch.equal(hp, par.cpu()), S
             w = min(S, 4096)
             assert np.array_equal(hp[:, :, :w].numpy(), O.encode(O.MSR_SPARSE, n, k, 14, x[:, :, :w]))
+            assert np.array_equal(hp[:, :, S - w:].numpy(), O.encode(O.MSR_SPARSE, n, k, 14, x[:, :, S - w:]))
     finally:
         pm.pmrc_destroy(code)
 

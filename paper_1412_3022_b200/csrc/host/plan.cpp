@@ -58,6 +58,16 @@ static std::string source_key(const std::string &src) {
   return buf;
 }
 
+// Structure statistics for resolve_options (groups, stages, supports, clustering, group costs,
+// shared memory per warp): none depends on the XOR networks' common-subexpression elimination, so
+// the probes generate without it (the expensive part of a generation)
+static void probe(const PlanSpec &p, GenOptions o, GenStats &st) {
+  o.cse = false;
+  o.cse_restarts = 1;
+  o.enc_restarts = 1;
+  (void)generate_source(p, o, st);
+}
+
 static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
   GenOptions oo = o;
   {
@@ -67,7 +77,7 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     GenOptions p0 = oo;
     if (p0.layout < 0) p0.layout = 0;
     GenStats w0;
-    (void)generate_source(p, p0, w0);
+    probe(p, p0, w0);
     if (o.auto_wide && p.w != 16 && w0.clustered && w0.max_stages >= 3 && p.outputs.size() > 8 && oo.team == 2 &&
         oo.max_rows == 8) {
       oo.max_rows = 16;
@@ -92,7 +102,7 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     GenOptions p1 = oo;
     if (p1.layout < 0) p1.layout = 0;
     GenStats w1;
-    (void)generate_source(p, p1, w1);
+    probe(p, p1, w1);
     if (w1.clustered) oo.dyn = 2;
   }
   if (p.w == 16) {  // 16 planes per row: groups of 4 rows (2 per warp), stages of <= 8 blocks of 2 KiB
@@ -103,7 +113,7 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     // group-specialised CTAs when the groups tile the 148 SMs with <= 10% left idle
     GenStats g0;
     oo.layout = 0;
-    (void)generate_source(p, oo, g0);
+    probe(p, oo, g0);
     const int G = std::max(1, g0.groups), sms = 148;
     oo.layout = (G <= sms && (sms % G) * 10 <= sms) ? 1 : 0;
     // unequal groups: apportion CTAs by cost (layout 2), unless the dynamic schedule balances them
@@ -114,7 +124,7 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     // stealing schedule puts those SMs to work as visitors (GF(2^16) k=8 encode, 14 groups:
     // 767 -> 822 GB/s); with <= 3 idle SMs static ranges measured better (GF(2^8) k=8: 7 groups)
     GenStats g2;
-    (void)generate_source(p, oo, g2);
+    probe(p, oo, g2);
     // ... and single-group plans of >= 3 stages (parity-node repair, 98 blocks in 7 stages: 0.405 ->
     // 0.387 ms; one-stage single-group plans, RS encode and systematic-node repair, measured slower)
     oo.dyn = (oo.layout == 1 && ((g2.groups > 1 && 148 % g2.groups >= 4) || (g2.groups == 1 && g2.max_stages >= 3)))
@@ -126,12 +136,12 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     oo.nbuf = 2;
   }
   // warps per CTA from the shared-memory budget (2 stage buffers of in_block KiB per team)
-  GenStats probe;
-  (void)generate_source(p, oo, probe);
+  GenStats pr;
+  probe(p, oo, pr);
   // 225 KiB of stage buffers (+ 1 KiB alignment reservation + the schedule slots <= 227 KiB): 16 warps
   // (8 teams of 2) with the k=8 encode's 14-block stages (224 KiB)
   int budget = o.smem_kib > 0 ? o.smem_kib * 1024 : 225 * 1024;
-  int w = std::max(1, std::min(32, budget / std::max(1, probe.smem_per_warp)));
+  int w = std::max(1, std::min(32, budget / std::max(1, pr.smem_per_warp)));
   // 16 warps when they fit: measured against 12 (the previous default, whose 220 KiB budget left the
   // encode at 12): MSR k=8 encode 0.528 -> 0.501 ms, MBR k=8 0.597 -> 0.568, parity-node repair
   // 0.387 -> 0.358, GF(2^16) k=8 1.359 -> 1.218, RS 0.345 -> 0.340; MSR k=4 and vanilla unchanged;

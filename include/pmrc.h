@@ -184,7 +184,10 @@ int pmrc_rt_plan_blob(pmrc_code *c, int op, int lost_id, const int *ids, int n_i
 
 /* Per-stripe failure patterns in ONE launch (config 4 as BASELINE.json states it; the
  * initialisation "depends on the failure pattern but can be reused across stripes"): stripe t has
- * its own pattern, run by the runtime-coefficient kernel (GF(2^8) codes).  nodes[i] (i < n) is node
+ * its own pattern, run by the runtime-coefficient kernel (GF(2^8) codes).  Under PMRC_PLAN_AUTO a
+ * stripe whose pattern has its generated kernel loaded (pmrc_plan_prepare) runs that kernel instead
+ * (one launch per run of consecutive stripes with that pattern, before the runtime launch of the
+ * rest); PMRC_PLAN_RUNTIME keeps every stripe on the runtime kernel.  nodes[i] (i < n) is node
  * i's piece region (stripe 0 + stripe stride, as pmrc_cregion elsewhere); only the regions a
  * stripe's pattern reads are touched (and validated).  Patterns are cached on the handle by id set.
  *
@@ -234,8 +237,8 @@ int pmrc_set_max_ctas(pmrc_code *c, int max_ctas);
  * (the default for every non-PDL kernel) complete before the launch starts.  When the preceding
  * work may trigger early (another handle with independent launches on, a PDL-enabled library
  * kernel), separate the two with an event wait or a non-PDL launch.  The batch calls
- * (pmrc_decode_batch / pmrc_repair_batch) run per-stripe patterns in ONE launch and need none of
- * this.  on = 0 (default): ordinary stream order.  Synchronises the device and drops the handle's
+ * (pmrc_decode_batch / pmrc_repair_batch) run the non-promoted per-stripe patterns in ONE launch
+ * and need none of this.  on = 0 (default): ordinary stream order.  Synchronises the device and drops the handle's
  * built kernels (rebuilt on next use).  PMRC_EINVAL for other values. */
 int pmrc_set_independent_launches(pmrc_code *c, int on);
 

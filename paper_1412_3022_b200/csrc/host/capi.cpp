@@ -1302,21 +1302,55 @@ static int check_node_regions(const pmrc_code *c, const pmrc_cregion *nodes, con
 }
 
 // shared tail of the batch calls: per-stripe keys -> specs -> runtime plans of one shape -> launch
+// jkeys[t] / jids[t]: the single-call plan key of stripe t's pattern and its node ids in slot order
+// (sorted); under PMRC_PLAN_AUTO a stripe whose pattern has a loaded JIT kernel (pmrc_plan_prepare,
+// earlier single calls under JIT) runs that kernel (runs of consecutive stripes of one pattern in
+// one launch, the node regions offset to the run's first stripe), the rest one runtime launch.
 static int run_batch(pmrc_code *c, const std::vector<std::string> &keys, const std::vector<const PlanSpec *> &specs,
+                     const std::vector<std::string> &jkeys, const std::vector<std::vector<int>> &jids,
                      const pmrc_cregion *nodes, uint64_t out_ptr, uint64_t out_stride, size_t S, size_t stripes,
                      void *stream) {
   const int n = c->def.n;
+  std::vector<char> jit(stripes, 0);
+  if (c->policy == PMRC_PLAN_AUTO && !c->dry)
+    for (size_t t = 0; t < stripes; t++) jit[t] = specs[t] && c->plans.count(jkeys[t]);
   int max_out = 0;
-  for (const PlanSpec *sp : specs)
-    if (sp) max_out = std::max(max_out, (int)sp->outputs.size());
-  if (!max_out || !S) return PMRC_OK;  // nothing to compute in any stripe
+  for (size_t t = 0; t < stripes; t++)
+    if (specs[t] && !jit[t]) max_out = std::max(max_out, (int)specs[t]->outputs.size());
+  const bool any_jit = std::find(jit.begin(), jit.end(), 1) != jit.end();
+  if (!S || (!max_out && !any_jit)) return PMRC_OK;  // nothing to compute in any stripe
+  int rc = ensure_device(c);
+  if (rc) return rc;
+  std::string err;
+  for (size_t t0 = 0; t0 < stripes;) {
+    if (!jit[t0]) {
+      t0++;
+      continue;
+    }
+    size_t t1 = t0 + 1;
+    while (t1 < stripes && jit[t1] && jkeys[t1] == jkeys[t0]) t1++;
+    Kernel *K = c->plans[jkeys[t0]].get();
+    const std::vector<int> &ids = jids[t0];
+    std::vector<uint64_t> ptrs(ids.size() + 1), strides(ids.size() + 1);
+    for (size_t q = 0; q < ids.size(); q++) {
+      ptrs[q] = (uint64_t)(uintptr_t)nodes[ids[q]].ptr + t0 * nodes[ids[q]].stripe_stride;
+      strides[q] = nodes[ids[q]].stripe_stride;
+    }
+    ptrs[ids.size()] = out_ptr + t0 * out_stride;
+    strides[ids.size()] = out_stride;
+    if (K->pace) c->traced = K;
+    rc = launch_kernel(*K, ptrs.data(), strides.data(), S, t1 - t0, stream, err, c->max_ctas);
+    if (rc) return fail(rc, err);
+    t0 = t1;
+  }
+  if (!max_out) return PMRC_OK;  // nothing left for the runtime kernel
   const pmrc_rt::RlcShape sh = rt_shape(max_out, c->gen);
   std::vector<RtPlan *> plans;
   std::map<std::string, uint16_t> idx;
   std::vector<uint16_t> stripe_plan(stripes);
   for (size_t t = 0; t < stripes; t++) {
-    if (!specs[t]) {
-      stripe_plan[t] = 0xFFFF;  // nothing to compute in this stripe
+    if (!specs[t] || jit[t]) {
+      stripe_plan[t] = 0xFFFF;  // nothing to compute in this stripe (or done by its JIT kernel)
       continue;
     }
     auto it = idx.find(keys[t]);
@@ -1337,9 +1371,6 @@ static int run_batch(pmrc_code *c, const std::vector<std::string> &keys, const s
   }
   ptrs[n] = out_ptr;
   strides[n] = out_stride;
-  int rc = ensure_device(c);
-  if (rc) return rc;
-  std::string err;
   rc = rt_launch(plans, stripe_plan.data(), ptrs.data(), strides.data(), n + 1, S, stripes, sh, stream, c->max_ctas,
                  err);
   if (rc) return fail(rc, err);
@@ -1372,7 +1403,8 @@ int pmrc_decode_batch(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_
     ~NoEvict() { c->no_evict = false; }
   } guard{c};
   c->no_evict = true;
-  std::vector<std::string> keys(stripes);
+  std::vector<std::string> keys(stripes), jkeys(stripes);
+  std::vector<std::vector<int>> jids(stripes);
   std::vector<const PlanSpec *> specs(stripes);
   std::vector<char> used(D.n, 0);
   std::vector<int> slot_of(D.n);
@@ -1383,6 +1415,8 @@ int pmrc_decode_batch(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_
     std::vector<int> s(ids, ids + n_surv);
     std::sort(s.begin(), s.end());
     keys[t] = ids_key("decn", s.data(), n_surv, 0);
+    jkeys[t] = ids_key("dec", s.data(), n_surv, 0);  // pmrc_decode's plan of this survivor set
+    jids[t] = s;
     std::vector<int> so(n_surv);
     for (int q = 0; q < n_surv; q++) so[q] = s[q];  // slot = node id
     int rc = get_spec(c, keys[t], [&](PlanSpec &sp) { return decode_spec(c, s.data(), n_surv, so.data(), D.n, D.n + 1,
@@ -1397,7 +1431,8 @@ int pmrc_decode_batch(pmrc_code *c, const int *surv_ids, int n_surv, const pmrc_
   int rc = check_node_regions(c, nodes, used, stripes);
   if (!rc) rc = check_region(data_out, (size_t)D.B * S, stripes);
   if (rc) return fail(rc, "bad region");
-  return run_batch(c, keys, specs, nodes, (uint64_t)(uintptr_t)data_out, (uint64_t)D.B * S, S, stripes, stream);
+  return run_batch(c, keys, specs, jkeys, jids, nodes, (uint64_t)(uintptr_t)data_out, (uint64_t)D.B * S, S, stripes,
+                   stream);
 }
 
 int pmrc_repair_batch(pmrc_code *c, const int *lost_ids, const int *helper_ids, int n_helpers, const pmrc_cregion *nodes,
@@ -1425,7 +1460,8 @@ int pmrc_repair_batch(pmrc_code *c, const int *lost_ids, const int *helper_ids, 
     ~NoEvict() { c->no_evict = false; }
   } guard{c};
   c->no_evict = true;
-  std::vector<std::string> keys(stripes);
+  std::vector<std::string> keys(stripes), jkeys(stripes);
+  std::vector<std::vector<int>> jids(stripes);
   std::vector<const PlanSpec *> specs(stripes);
   std::vector<char> used(D.n, 0);
   for (size_t t = 0; t < stripes; t++) {
@@ -1437,6 +1473,8 @@ int pmrc_repair_batch(pmrc_code *c, const int *lost_ids, const int *helper_ids, 
     std::vector<int> H(ids, ids + n_helpers);
     std::sort(H.begin(), H.end());
     keys[t] = ids_key("repn", H.data(), n_helpers, f);
+    jkeys[t] = ids_key("rep", H.data(), n_helpers, f);  // pmrc_repair's plan of this (f, H)
+    jids[t] = H;
     rc = get_spec(c, keys[t], [&](PlanSpec &sp) {
       return repair_spec(c, f, H.data(), n_helpers, H.data(), D.n, D.n + 1, sp);  // slot = node id
     }, &specs[t]);
@@ -1447,8 +1485,8 @@ int pmrc_repair_batch(pmrc_code *c, const int *lost_ids, const int *helper_ids, 
   int rc = check_node_regions(c, nodes, used, stripes);
   if (!rc) rc = check_region(out_piece.ptr, out_piece.stripe_stride, stripes);
   if (rc) return fail(rc, "bad region");
-  return run_batch(c, keys, specs, nodes, (uint64_t)(uintptr_t)out_piece.ptr, out_piece.stripe_stride, S, stripes,
-                   stream);
+  return run_batch(c, keys, specs, jkeys, jids, nodes, (uint64_t)(uintptr_t)out_piece.ptr, out_piece.stripe_stride, S,
+                   stripes, stream);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -247,3 +247,47 @@ def test_new_plan_used_on_another_stream_right_away():
             assert torch.equal(o[:, miss], st.data[:, miss])
     finally:
         st.close()
+
+
+def test_batch_runs_promoted_patterns_on_their_generated_kernels():
+    # "the JIT kernels stay as a cache for hot patterns": under AUTO, stripes whose pattern was
+    # promoted (pmrc_plan_prepare) run its generated kernel, one launch per run of consecutive
+    # stripes with that pattern; the other stripes share one runtime launch; same bytes either way
+    k, n, S, stripes = 8, 16, 4096 + 512, 7
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=71)
+    try:
+        st.encode()
+        A = (15, [i for i in range(15) if i != 9])           # parity node, helpers without node 9
+        B = (6, [i for i in range(n) if i not in (6, 15)])   # systematic node
+        C = (11, [i for i in range(n) if i not in (11, 2)])
+        reps = [A, A, A, B, A, A, C]
+        da, db, dc = [0, 1, 4, 5, 9, 12, 14, 15], [2, 3, 8, 9, 10, 11, 12, 13], list(range(8, 16))
+        decs = [da, da, db, dc, dc, da, db]
+        pm.pmrc_plan_prepare(st.code, 1, A[0], A[1])
+        pm.pmrc_plan_prepare(st.code, 1, C[0], C[1])
+        pm.pmrc_plan_prepare(st.code, 0, 0, da)
+        pm.pmrc_plan_prepare(st.code, 0, 0, dc)
+        nodes = st.nodes()
+        for policy, launches in ((pm.PMRC_PLAN_AUTO, (4, 4)), (pm.PMRC_PLAN_RUNTIME, (1, 1))):
+            pm.pmrc_set_plan_policy(st.code, policy)
+            out = torch.full((stripes, st.alpha, S), 0x3C, dtype=torch.uint8, device=DEV)
+            l0 = pm.pmrc_launch_count()
+            pm.pmrc_repair_batch(st.code, [f for f, _ in reps], [list(reversed(H)) for _, H in reps], nodes,
+                                 (out.data_ptr(), st.alpha * S), S, stripes, st.stream)
+            torch.cuda.synchronize()
+            assert pm.pmrc_launch_count() - l0 == launches[0], policy   # A x2 runs + C, then B
+            for t, (f, _) in enumerate(reps):
+                assert torch.equal(out[t], st.piece_tensor(f)[t]), (policy, t, f)
+            dec = torch.full_like(st.data, 0xA5)
+            l0 = pm.pmrc_launch_count()
+            nw = pm.pmrc_decode_batch(st.code, decs, nodes, dec.data_ptr(), S, stripes, st.stream)
+            torch.cuda.synchronize()
+            assert pm.pmrc_launch_count() - l0 == launches[1], policy   # da x2 runs + dc, then db
+            for t, ids in enumerate(decs):
+                miss = _missing(st, ids)
+                keep = [b for b in range(st.B) if b not in miss]
+                assert nw[t] == len(miss)
+                assert torch.equal(dec[t, miss], st.data[t, miss]), (policy, t)
+                assert bool((dec[t, keep] == 0xA5).all()), (policy, t)
+    finally:
+        st.close()

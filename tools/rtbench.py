@@ -172,7 +172,56 @@ def config4_batch(steps):
           "ms": round(ms_d, 4), "GBps": round(j.stripes * j.B * S / ms_d / 1e6, 1),
           "host_init_ms": round(init_d * 1e3, 2), "hbm_bytes": db, "hbm_frac": round(db / hb / (ms_d * 1e-3), 3),
           "rt_alu_frac": round(d_ops / ALU / (ms_d * 1e-3), 3)})
+    if os.environ.get("RTB_PROMOTED", "1") == "1":
+        promoted(j, reps, decs, nodes, out, dec, rb, db, hb, steps)
     return j
+
+
+def promoted(j, reps, decs, nodes, out, dec, rb, db, hb, steps):
+    """The same batch calls after every pattern was promoted to its generated kernel (AUTO policy:
+    one JIT launch per stripe, no runtime launch), without and with independent (PDL) launches."""
+    S, a, k = j.S, j.a, j.k
+    pats = [("repair", f, H) for f, H in reps] + [("decode", ids) for ids in decs]
+    for indep in (0, 1):
+        t0 = time.perf_counter()
+        res = pm.prepare_plans(0, k, j.d, j.n, pats, independent=bool(indep))   # NVRTC, parallel
+        prep = time.perf_counter() - t0
+        pm.pmrc_set_independent_launches(j.code, indep)
+        t0 = time.perf_counter()
+        for (pt, rc) in res:
+            if rc == pm.PMRC_OK:
+                if pt[0] == "repair":
+                    pm.pmrc_plan_prepare(j.code, 1, pt[1], pt[2])
+                else:
+                    pm.pmrc_plan_prepare(j.code, 0, 0, pt[1])
+        load = time.perf_counter() - t0
+        out.zero_()
+        dec.zero_()
+        l0 = pm.pmrc_launch_count()
+        pm.pmrc_repair_batch(j.code, [f for f, _ in reps], [H for _, H in reps], nodes, (out.data_ptr(), a * S), S,
+                             j.stripes, j.st)
+        lr = pm.pmrc_launch_count() - l0
+        l0 = pm.pmrc_launch_count()
+        pm.pmrc_decode_batch(j.code, decs, nodes, dec.data_ptr(), S, j.stripes, j.st)
+        ld = pm.pmrc_launch_count() - l0
+        torch.cuda.synchronize()
+        ok_r = all(bool(torch.equal(out[t], j.piece_t(f)[t])) for t, (f, _) in enumerate(reps))
+        ok_d = True
+        for t, ids in enumerate(decs):
+            miss = [i * a + x for i in range(k) if i not in ids for x in range(a)]
+            if miss:
+                ok_d &= bool(torch.equal(dec[t, miss], j.data[t, miss]))
+        ms_r = timed(lambda: pm.pmrc_repair_batch(j.code, [f for f, _ in reps], [H for _, H in reps], nodes,
+                                                  (out.data_ptr(), a * S), S, j.stripes, j.st), steps)
+        ms_d = timed(lambda: pm.pmrc_decode_batch(j.code, decs, nodes, dec.data_ptr(), S, j.stripes, j.st), steps)
+        tag = "promoted_pdl" if indep else "promoted"
+        emit({"op": "repair_batch", "config": "config4", "plans": tag, "stripes": j.stripes, "launches": lr,
+              "bit_exact": ok_r, "ms": round(ms_r, 4), "GBps_repaired": round(j.stripes * a * S / ms_r / 1e6, 1),
+              "nvrtc_s": round(prep, 2), "load_s": round(load, 2), "hbm_frac": round(rb / hb / (ms_r * 1e-3), 3)})
+        emit({"op": "decode_batch", "config": "config4", "plans": tag, "stripes": j.stripes, "launches": ld,
+              "bit_exact": ok_d, "ms": round(ms_d, 4), "GBps": round(j.stripes * j.B * S / ms_d / 1e6, 1),
+              "hbm_frac": round(db / hb / (ms_d * 1e-3), 3)})
+    pm.pmrc_set_independent_launches(j.code, 0)
 
 
 def single(j, steps):

@@ -120,12 +120,13 @@ def _precompile_decode(args):
 
 def precompile(configs=PRECOMPILE, clean=True):
     """NVRTC-compile the encode kernels of `configs` into paper_1412_3022_b200/kcache (no GPU).
-    clean=True first drops cubins of earlier generator versions (the cache is keyed by source)."""
+    clean=True first drops cubins of earlier generator versions (the cache is keyed by source) and the
+    plan index of earlier library builds (its key includes the build)."""
     from multiprocessing import get_context
     kdir = os.path.join(HERE, "kcache")
     if clean and os.path.isdir(kdir):
         for f in os.listdir(kdir):
-            if f.endswith(".cubin"):
+            if f.endswith(".cubin") or f.endswith(".meta"):
                 os.remove(os.path.join(kdir, f))
     with get_context("spawn").Pool(min(len(configs), os.cpu_count() or 4)) as pool:
         res = pool.map(_precompile_one, configs)

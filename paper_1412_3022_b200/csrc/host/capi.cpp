@@ -45,7 +45,8 @@ struct pmrc_code {
   PlanSpec enc_spec;
   Kernel enc;
   bool enc_built = false;
-  GenStats enc_stats;
+  mutable GenStats enc_stats;       // XOR-program statistics of the encode (pmrc_info; computed on first use)
+  mutable bool enc_stats_ok = false;
   std::map<std::string, std::unique_ptr<Kernel>> plans;  // decode / repair / project / combine
   std::map<std::string, int> plan_err;                   // cached failures (ESINGULAR)
   std::map<std::string, int> plan_meta;                  // e.g. blocks written by a decode plan
@@ -354,7 +355,6 @@ int pmrc_create(pmrc_code **out, int kind, int k, int d, int n, int w) {
   c->enc_spec.n_slots = 2;
   for (int i = 0; i < D.B; i++) c->enc_spec.inputs.push_back({{{0, i, 1}}});
   for (int r = 0; r < D.P; r++) c->enc_spec.outputs.push_back({1, r});
-  (void)generate_source(c->enc_spec, enc_gen(c.get()), c->enc_stats);  // XOR-program statistics
   // compile now if a device is present (the paper's initialization); else on first use
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) {
@@ -399,6 +399,10 @@ int pmrc_info(const pmrc_code *c, pmrc_info_t *o) {
   o->nnz = (int)nnz;
   o->zero_pct = Apat.a.empty() ? 0.0 : 100.0 * (double)(Apat.a.size() - nnz) / (double)Apat.a.size();
   o->repair_complete = D.repair_complete ? 1 : 0;
+  if (!c->enc_stats_ok) {
+    (void)generate_source(c->enc_spec, enc_gen(c), c->enc_stats);
+    c->enc_stats_ok = true;
+  }
   o->xor_ops = c->enc_stats.xor2;
   o->xor_ops_naive = c->enc_stats.naive_lop3;
   return PMRC_OK;

@@ -58,6 +58,120 @@ static std::string source_key(const std::string &src) {
   return buf;
 }
 
+// Plan index: kcache/<plan key>.meta maps (plan, generator options, library build) to the source key
+// of the plan's cubin plus the generator's statistics and resolved launch options, so that a plan
+// built before loads its cubin without generating its source again (generation is the seconds of a
+// plan build; NVRTC is skipped by the cubin cache).  The build id is part of the key: a rebuilt
+// library never reuses another build's index (its cubins, keyed by source, stay valid).
+static const char kBuildId[] = __DATE__ " " __TIME__;
+
+#define PMRC_GEN_FIELDS(X)                                                                                     \
+  X(max_rows) X(in_block) X(stage_even) X(warps) X(tpb) X(cse) X(sync_groups) X(dyn) X(pdl) X(smem_kib)         \
+  X(dyn_static) X(cta_sync) X(chunk_loop) X(team) X(ld_hint) X(fold) X(layout) X(grid_ctas) X(tr_balance)       \
+  X(balance_ranks) X(cluster_wide) X(even_groups) X(auto_wide16) X(auto_wide) X(enc_restarts) X(cse_restarts)   \
+  X(sched) X(l2_shared) X(ws_prod) X(ws) X(own_first) X(nbuf) X(tr_unroll) X(fence) X(net_even) X(net_in)       \
+  X(trace) X(pace_lag) X(l0_sync) X(rt_groups)
+#define PMRC_COUNT(m) +1
+static_assert(0 PMRC_GEN_FIELDS(PMRC_COUNT) == 40 && sizeof(GenOptions) == 132,
+              "GenOptions changed: list every field in PMRC_GEN_FIELDS (the plan index key)");
+#undef PMRC_COUNT
+
+namespace {
+struct Fnv {
+  uint64_t h = 1469598103934665603ull;
+  void add(const void *p, size_t n) {
+    const unsigned char *b = (const unsigned char *)p;
+    for (size_t i = 0; i < n; i++) h = (h ^ b[i]) * 1099511628211ull;
+  }
+  template <class T>
+  void v(T x) {
+    add(&x, sizeof x);
+  }
+};
+}  // namespace
+
+static std::string plan_key(const PlanSpec &p, const GenOptions &o) {
+  Fnv f;
+  f.add(kBuildId, sizeof kBuildId);
+  f.v(p.n_slots);
+  f.v(p.w);
+  f.v(p.inputs.size());
+  for (const auto &in : p.inputs) {
+    f.v(in.terms.size());
+    for (const auto &t : in.terms) {
+      f.v(t.slot);
+      f.v(t.blk);
+      f.v(t.coef);
+    }
+  }
+  f.v(p.outputs.size());
+  for (const auto &out : p.outputs) {
+    f.v(out.slot);
+    f.v(out.blk);
+  }
+  f.v(p.A.r);
+  f.v(p.A.c);
+  f.add(p.A.a.data(), p.A.a.size());
+  f.v(p.A16.size());
+  f.add(p.A16.data(), p.A16.size() * sizeof(uint16_t));
+#define X(m) f.v(o.m);
+  PMRC_GEN_FIELDS(X)
+#undef X
+  char buf[40];
+  snprintf(buf, sizeof buf, "%016llx", (unsigned long long)f.h);
+  return buf;
+}
+
+struct PlanMeta {
+  std::string src_key;
+  GenStats st;
+  GenOptions oo;  // resolved: tpb, chunk_loop, layout, grid_ctas, warps, team, pdl are read back
+  bool dyn_on = false, dyn_full = false;
+};
+
+static void write_meta(const std::string &dir, const std::string &key, const PlanMeta &m) {
+  if (dir.empty()) return;
+  mkdir(dir.c_str(), 0755);
+  const std::string path = dir + "/" + key + ".meta", tmp = path + ".tmp" + std::to_string((long)getpid());
+  {
+    std::ofstream f(tmp);
+    const GenStats &t = m.st;
+    const GenOptions &o = m.oo;
+    f << "pmrc-plan-meta 1\n"
+      << m.src_key << "\n"
+      << t.groups << " " << t.xor2 << " " << t.naive_lop3 << " " << t.xor2_naive << " " << t.transposes << " "
+      << t.loads << " " << t.smem_per_warp << " " << t.max_stages << " " << t.max_support_rows << " "
+      << (int)t.clustered << " " << std::hexfloat << t.group_cost_ratio << std::defaultfloat << "\n"
+      << o.tpb << " " << o.chunk_loop << " " << o.layout << " " << o.grid_ctas << " " << o.warps << " " << o.team
+      << " " << o.pdl << " " << (int)m.dyn_on << " " << (int)m.dyn_full << "\n";
+    if (!f) {
+      remove(tmp.c_str());
+      return;
+    }
+  }
+  rename(tmp.c_str(), path.c_str());
+}
+
+static bool read_meta(const std::string &dir, const std::string &key, PlanMeta &m) {
+  if (dir.empty()) return false;
+  std::ifstream f(dir + "/" + key + ".meta");
+  std::string tag;
+  int ver = 0, cl = 0, don = 0, dfull = 0;
+  if (!(f >> tag >> ver) || tag != "pmrc-plan-meta" || ver != 1) return false;
+  GenStats &t = m.st;
+  GenOptions &o = m.oo;
+  std::string ratio;
+  if (!(f >> m.src_key >> t.groups >> t.xor2 >> t.naive_lop3 >> t.xor2_naive >> t.transposes >> t.loads >>
+        t.smem_per_warp >> t.max_stages >> t.max_support_rows >> cl >> ratio))
+    return false;
+  t.clustered = cl != 0;
+  t.group_cost_ratio = strtod(ratio.c_str(), nullptr);
+  if (!(f >> o.tpb >> o.chunk_loop >> o.layout >> o.grid_ctas >> o.warps >> o.team >> o.pdl >> don >> dfull)) return false;
+  m.dyn_on = don != 0;
+  m.dyn_full = dfull != 0;
+  return true;
+}
+
 // Structure statistics for resolve_options (groups, stages, supports, clustering, group costs,
 // shared memory per warp): none depends on the XOR networks' common-subexpression elimination, so
 // the probes generate without it (the expensive part of a generation)
@@ -156,19 +270,21 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
 }
 
 // NVRTC compile (no GPU needed) with the on-disk cache; returns the cubin.
+static bool cached_cubin(const std::string &dir, const std::string &src_key, std::vector<char> &cubin) {
+  if (dir.empty()) return false;
+  std::ifstream f(dir + "/" + src_key + ".cubin", std::ios::binary);
+  if (!f) return false;
+  cubin.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+  return !cubin.empty();
+}
+
 static int compile_cubin(const std::string &src, std::vector<char> &cubin, bool &from_cache, std::string &err) {
   from_cache = false;
   const std::string dir = cache_dir();
   const std::string path = dir.empty() ? "" : dir + "/" + source_key(src) + ".cubin";
-  if (!path.empty()) {
-    std::ifstream f(path, std::ios::binary);
-    if (f) {
-      cubin.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
-      if (!cubin.empty()) {
-        from_cache = true;
-        return PMRC_OK;
-      }
-    }
+  if (cached_cubin(dir, source_key(src), cubin)) {
+    from_cache = true;
+    return PMRC_OK;
   }
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, src.c_str(), "pmrc_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
@@ -209,22 +325,62 @@ std::string plan_source(const PlanSpec &p, const GenOptions &o, GenStats &st) {
   return generate_source(p, resolve_options(p, o), st);
 }
 
+static bool dyn_on_of(const std::string &src) { return src.find("u32 *__restrict__ dyn)") != std::string::npos; }
+static bool dyn_full_of(const std::string &src) { return src.find("for (u32 hop = 0;") != std::string::npos; }
+
 int precompile_kernel(const PlanSpec &p, const GenOptions &o, std::string &err) {
-  GenOptions oo = resolve_options(p, o);
-  GenStats st;
-  std::string src = generate_source(p, oo, st);
+  const std::string dir = cache_dir(), key = plan_key(p, o);
+  PlanMeta m;
   std::vector<char> cubin;
+  if (read_meta(dir, key, m) && cached_cubin(dir, m.src_key, cubin)) return PMRC_OK;
+  m.oo = resolve_options(p, o);
+  std::string src = generate_source(p, m.oo, m.st);
   bool cached = false;
-  return compile_cubin(src, cubin, cached, err);
+  int rc = compile_cubin(src, cubin, cached, err);
+  if (rc) return rc;
+  m.src_key = source_key(src);
+  m.dyn_on = dyn_on_of(src);
+  m.dyn_full = dyn_full_of(src);
+  write_meta(dir, key, m);
+  return PMRC_OK;
 }
 
 int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string &err) {
   auto t0 = std::chrono::steady_clock::now();
   k = Kernel();
-  GenOptions oo = resolve_options(p, o);
-  k.source = generate_source(p, oo, k.stats);
-  if (const char *dd = getenv("PMRC_DUMP")) {  // diagnostics: keep the generated source of every plan
-    std::ofstream(std::string(dd) + "/" + source_key(k.source) + ".cu") << k.source;
+  const std::string dir = cache_dir(), key = plan_key(p, o);
+  PlanMeta m;
+  std::vector<char> cubin;
+  bool cached = false;
+  // a plan built before (same spec, options, library build): cubin and launch parameters from the
+  // index, no generation (diagnostic builds, PMRC_DUMP / trace / pacing, always generate)
+  const bool diag = getenv("PMRC_DUMP") || o.trace || o.pace_lag > 0;
+  GenOptions oo;
+  if (!diag && read_meta(dir, key, m) && cached_cubin(dir, m.src_key, cubin)) {
+    cached = true;
+    oo = o;
+    oo.tpb = m.oo.tpb;
+    oo.chunk_loop = m.oo.chunk_loop;
+    oo.layout = m.oo.layout;
+    oo.grid_ctas = m.oo.grid_ctas;
+    oo.warps = m.oo.warps;
+    oo.team = m.oo.team;
+    oo.pdl = m.oo.pdl;
+    k.stats = m.st;
+  } else {
+    oo = resolve_options(p, o);
+    k.source = generate_source(p, oo, k.stats);
+    if (const char *dd = getenv("PMRC_DUMP")) {  // diagnostics: keep the generated source of every plan
+      std::ofstream(std::string(dd) + "/" + source_key(k.source) + ".cu") << k.source;
+    }
+    int crc = compile_cubin(k.source, cubin, cached, err);
+    if (crc) return crc;
+    m.src_key = source_key(k.source);
+    m.st = k.stats;
+    m.oo = oo;
+    m.dyn_on = dyn_on_of(k.source);
+    m.dyn_full = dyn_full_of(k.source);
+    if (!diag) write_meta(dir, key, m);
   }
   k.n_slots = std::max(1, p.n_slots);
   k.n_groups = std::max(1, k.stats.groups);
@@ -236,10 +392,6 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
   k.teams = std::max(1, oo.warps / std::max(1, oo.team));
   k.pdl = oo.pdl > 0;
   k.smem = (size_t)k.stats.smem_per_warp * oo.warps;
-  std::vector<char> cubin;
-  bool cached = false;
-  int crc = compile_cubin(k.source, cubin, cached, err);
-  if (crc) return crc;
   auto t1 = std::chrono::steady_clock::now();
   k.compile_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   k.from_cache = cached;
@@ -287,7 +439,7 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
       return PMRC_ENOMEM;
     }
   }
-  if (k.source.find("u32 *__restrict__ dyn)") != std::string::npos) {
+  if (m.dyn_on) {
     // dynamic schedule: a ring of counter slots, one per launch (the last team of a group resets
     // its slot), so launches of this plan on different streams do not share counters
     const size_t bytes = (size_t)kDynSlots * 2 * k.n_groups * sizeof(uint32_t);
@@ -298,7 +450,7 @@ int build_kernel(const PlanSpec &p, const GenOptions &o, Kernel &k, std::string 
       return PMRC_ENOMEM;
     }
     k.dyn_on = true;
-    k.dyn_full = k.source.find("for (u32 hop = 0;") != std::string::npos;
+    k.dyn_full = m.dyn_full;
   }
   return PMRC_OK;
 }

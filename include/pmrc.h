@@ -174,6 +174,19 @@ int pmrc_get_plan_policy(const pmrc_code *c);
  * calls with this pattern run it under PMRC_PLAN_AUTO (hot-pattern promotion).  Errors as
  * pmrc_decode / pmrc_repair. */
 int pmrc_plan_prepare(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids);
+/* Automatic promotion under PMRC_PLAN_AUTO (a pattern's initialisation is reused across the
+ * stripes that follow): once a decode / repair pattern has moved `bytes` of plan traffic (S x
+ * stripes x (input blocks + output blocks), summed over its single calls) on the runtime kernel, a
+ * host thread generates and NVRTC-compiles its kernel into the in-tree kernel cache while the calls
+ * keep running on the runtime kernel; the first call after that loads the cubin (milliseconds) and
+ * the pattern runs its generated kernel from then on.  Default 1 GiB; 0 disables.  Needs the kernel
+ * cache (PMRC_KCACHE not "off").  Batch calls use promoted patterns but do not count traffic.
+ * pmrc_destroy waits for compilations in flight. */
+int pmrc_set_auto_promotion(pmrc_code *c, unsigned long long bytes);
+/* Engine state of a decode (op 0) / repair (op 1) pattern on this handle: 0 runtime kernel (no
+ * generated kernel loaded), 1 promotion compiling, 2 promotion compiled (loaded by the next call),
+ * 3 generated kernel loaded.  Negative: error code. */
+int pmrc_plan_state(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids);
 
 /* The runtime-coefficient kernel's plan blob (u32 words; layout: csrc/rt/rlc.hpp RlcHdr) of a decode
  * (op 0, ids = survivors), repair (op 1, lost_id, ids = helpers) or encode (op 2) plan, built on the

@@ -26,7 +26,7 @@ EXPORTS = ["pmrc_create", "pmrc_destroy", "pmrc_info", "pmrc_matrix", "pmrc_layo
            "pmrc_encode_source", "pmrc_debug_counters", "pmrc_plan_source", "pmrc_plan_stats", "pmrc_apply", "pmrc_apply_stats", "pmrc_set_max_ctas",
            "pmrc_set_independent_launches", "pmrc_set_plan_policy", "pmrc_get_plan_policy", "pmrc_plan_prepare",
            "pmrc_decode_batch", "pmrc_repair_batch", "pmrc_decode_specific", "pmrc_decode_specific_scratch",
-           "pmrc_rt_plan_blob"]
+           "pmrc_rt_plan_blob", "pmrc_set_auto_promotion", "pmrc_plan_state"]
 
 
 class PmrcError(RuntimeError):
@@ -96,6 +96,8 @@ def lib():
             "pmrc_set_plan_policy": ([P, I], I),
             "pmrc_get_plan_policy": ([P], I),
             "pmrc_plan_prepare": ([P, I, I, IP, I], I),
+            "pmrc_set_auto_promotion": ([P, ctypes.c_ulonglong], I),
+            "pmrc_plan_state": ([P, I, I, IP, I], I),
             "pmrc_decode_batch": ([P, IP, I, ctypes.POINTER(pmrc_cregion), P, Z, Z, IP, P], I),
             "pmrc_repair_batch": ([P, IP, IP, I, ctypes.POINTER(pmrc_cregion), pmrc_region, Z, Z, P], I),
             "pmrc_decode_specific_scratch": ([P, Z, Z, ctypes.POINTER(ctypes.c_size_t)], I),
@@ -261,6 +263,24 @@ def pmrc_plan_prepare(code, op, lost_id, ids):
     """JIT-compile and keep the generated kernel of a decode (op 0) / repair (op 1) pattern."""
     arr, n = _ints(ids)
     _check(lib().pmrc_plan_prepare(code, op, lost_id, arr, n), "pmrc_plan_prepare")
+
+
+def pmrc_set_auto_promotion(code, nbytes):
+    """AUTO policy: compile a pattern's generated kernel in a host thread once it moved nbytes of
+    plan traffic on the runtime kernel (0 = off; default 1 GiB)."""
+    _check(lib().pmrc_set_auto_promotion(code, nbytes), "pmrc_set_auto_promotion")
+
+
+PLAN_RUNTIME_ONLY, PLAN_COMPILING, PLAN_COMPILED, PLAN_LOADED = 0, 1, 2, 3
+
+
+def pmrc_plan_state(code, op, lost_id, ids):
+    """0 runtime kernel only, 1 promotion compiling, 2 compiled (loads at the next call), 3 loaded."""
+    arr, n = _ints(ids)
+    rc = lib().pmrc_plan_state(code, op, lost_id, arr, n)
+    if rc < 0:
+        _check(rc, "pmrc_plan_state")
+    return rc
 
 
 def pmrc_decode_batch(code, surv_ids, nodes, data_out_ptr, S, stripes, stream=0):

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -9,6 +10,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../../include/pmrc.h"
@@ -63,6 +65,20 @@ struct pmrc_code {
   std::map<std::string, std::unique_ptr<PlanSpec>> specs;  // plan specs by key (null: nothing to compute)
   std::map<std::string, std::unique_ptr<RtPlan>> rt_plans; // runtime-coefficient plans by key + shape
   bool no_evict = false;       // a batch call holds pointers into the caches: no eviction meanwhile
+  // AUTO promotion of hot patterns (pmrc_set_auto_promotion): plan traffic run on the runtime
+  // kernel per single-call plan key; past promote_bytes a host thread compiles the pattern's
+  // generated kernel into the kernel cache, and the next call after it finished loads and runs it
+  unsigned long long promote_bytes = 1ull << 30;
+  std::map<std::string, unsigned long long> rt_traffic;
+  struct Promotion {
+    std::thread th;
+    std::atomic<int> state{1};  // 1 compiling, 2 compiled into the cache, 3 failed
+  };
+  std::map<std::string, std::unique_ptr<Promotion>> promos;
+  ~pmrc_code() {
+    for (auto &kv : promos)
+      if (kv.second->th.joinable()) kv.second->th.join();
+  }
 };
 
 namespace {
@@ -1010,6 +1026,48 @@ static int get_spec(pmrc_code *c, const std::string &key, Make make, const PlanS
   return PMRC_OK;
 }
 
+// Hot-pattern promotion under AUTO.  Traffic of a plan = S x stripes x (distinct input blocks +
+// outputs).  Once a pattern's runtime-kernel traffic reaches promote_bytes, a host thread
+// generates and NVRTC-compiles its kernel into the kernel cache (the calls keep running on the
+// runtime kernel meanwhile); the first call after that loads the cubin through the plan index
+// (milliseconds) and runs the generated kernel from then on.  Needs the kernel cache.
+static void maybe_promote(pmrc_code *c, const std::string &key, const PlanSpec &spec, unsigned long long cols) {
+  if (!c->promote_bytes || c->promos.count(key) || !kernel_cache_enabled()) return;
+  if (c->rt_traffic.size() > kMaxSpecs) c->rt_traffic.clear();
+  std::vector<std::pair<int, int>> blocks;
+  for (const auto &in : spec.inputs)
+    for (const auto &t : in.terms) blocks.push_back({t.slot, t.blk});
+  std::sort(blocks.begin(), blocks.end());
+  blocks.erase(std::unique(blocks.begin(), blocks.end()), blocks.end());
+  unsigned long long &tr = c->rt_traffic[key];
+  tr += cols * (unsigned long long)(blocks.size() + spec.outputs.size());
+  if (tr < c->promote_bytes) return;
+  auto pr = std::make_unique<pmrc_code::Promotion>();
+  pmrc_code::Promotion *pp = pr.get();
+  pr->th = std::thread([pp, sp = spec, g = c->gen]() {
+    std::string err;
+    pp->state = precompile_kernel(sp, g, err) == PMRC_OK ? 2 : 3;
+  });
+  c->promos[key] = std::move(pr);
+}
+
+// true when the pattern's promotion finished and its kernel is in the cache's plan index for the
+// handle's current options (then get_kernel loads it without generation or NVRTC)
+static bool promotion_done(pmrc_code *c, const std::string &key, const PlanSpec &spec) {
+  auto it = c->promos.find(key);
+  if (it == c->promos.end() || it->second->state.load() == 1) return false;
+  it->second->th.join();
+  const bool ok = it->second->state.load() == 2 && plan_indexed(spec, c->gen);
+  if (!ok) {
+    c->promos.erase(it);  // failed, or compiled for options changed since: account afresh
+    c->rt_traffic.erase(key);
+    return false;
+  }
+  c->promos.erase(it);
+  Kernel *K = nullptr;
+  return get_kernel(c, key, spec, &K) == PMRC_OK;
+}
+
 // Run a single plan over `stripes` stripes (slots of stripe 0 in ptrs, their strides).
 static int run_plan(pmrc_code *c, const std::string &key, const PlanSpec &spec, const uint64_t *ptrs,
                     const uint64_t *strides, size_t S, size_t stripes, void *stream) {
@@ -1018,7 +1076,9 @@ static int run_plan(pmrc_code *c, const std::string &key, const PlanSpec &spec, 
     Kernel *K = nullptr;
     return get_kernel(c, key, spec, &K);  // kDryRun (source / stats only)
   }
-  if (use_runtime(c, key)) {
+  bool rt = use_runtime(c, key);
+  if (rt && c->policy == PMRC_PLAN_AUTO && promotion_done(c, key, spec)) rt = false;
+  if (rt) {
     const pmrc_rt::RlcShape sh = rt_shape((int)spec.outputs.size(), c->gen);
     RtPlan *P = nullptr;
     int rc = get_rt_plan(c, key, spec, sh.R, sh.G, &P);
@@ -1028,6 +1088,7 @@ static int run_plan(pmrc_code *c, const std::string &key, const PlanSpec &spec, 
       if (rc) return rc;
       rc = rt_launch({P}, nullptr, ptrs, strides, spec.n_slots, S, stripes, sh, stream, c->max_ctas, err);
       if (rc) return fail(rc, err);
+      if (c->policy == PMRC_PLAN_AUTO) maybe_promote(c, key, spec, (unsigned long long)S * stripes);
       return PMRC_OK;
     }
     if (!(rc == PMRC_EUNSUPPORTED && c->policy == PMRC_PLAN_AUTO)) return rc;
@@ -1830,6 +1891,26 @@ int pmrc_rt_plan_blob(pmrc_code *c, int op, int lost_id, const int *ids_in, int 
   *n_words = P.blob.size();
   if (buf && cap >= P.blob.size()) memcpy(buf, P.blob.data(), P.blob.size() * 4);
   return PMRC_OK;
+}
+
+int pmrc_set_auto_promotion(pmrc_code *c, unsigned long long bytes) {
+  if (!c) return fail(PMRC_EINVAL, "NULL handle");
+  c->promote_bytes = bytes;
+  return PMRC_OK;
+}
+
+int pmrc_plan_state(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids) {
+  // 0: no generated kernel loaded (runtime kernel under AUTO), 1: promotion compiling,
+  // 2: promotion compiled (loaded at the next call), 3: generated kernel loaded
+  if (!c || !ids) return fail(PMRC_EINVAL, "NULL argument");
+  if (op != 0 && op != 1) return fail(PMRC_EINVAL, "op must be 0 (decode) or 1 (repair)");
+  std::vector<int> s(ids, ids + n_ids);
+  std::sort(s.begin(), s.end());
+  const std::string key = op == 0 ? ids_key("dec", s.data(), n_ids, 0) : ids_key("rep", s.data(), n_ids, lost_id);
+  if (c->plans.count(key)) return 3;
+  auto it = c->promos.find(key);
+  if (it == c->promos.end()) return 0;
+  return it->second->state.load() == 1 ? 1 : 2;
 }
 
 int pmrc_plan_prepare(pmrc_code *c, int op, int lost_id, const int *ids, int n_ids) {

@@ -325,6 +325,14 @@ std::string plan_source(const PlanSpec &p, const GenOptions &o, GenStats &st) {
   return generate_source(p, resolve_options(p, o), st);
 }
 
+bool kernel_cache_enabled() { return !cache_dir().empty(); }
+
+bool plan_indexed(const PlanSpec &p, const GenOptions &o) {
+  const std::string dir = cache_dir();
+  PlanMeta m;
+  return read_meta(dir, plan_key(p, o), m) && access((dir + "/" + m.src_key + ".cubin").c_str(), R_OK) == 0;
+}
+
 static bool dyn_on_of(const std::string &src) { return src.find("u32 *__restrict__ dyn)") != std::string::npos; }
 static bool dyn_full_of(const std::string &src) { return src.find("for (u32 hop = 0;") != std::string::npos; }
 

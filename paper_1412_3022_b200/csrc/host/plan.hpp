@@ -148,6 +148,10 @@ void free_kernel(Kernel &k);
 std::string plan_source(const PlanSpec &p, const GenOptions &o, GenStats &st);
 // Generate + NVRTC-compile into the kernel cache only (no GPU needed).
 int precompile_kernel(const PlanSpec &p, const GenOptions &o, std::string &err);
+// True when the kernel cache is enabled and its plan index holds this plan (same spec, options and
+// library build) with its cubin: build_kernel then loads it without generation or NVRTC.
+bool plan_indexed(const PlanSpec &p, const GenOptions &o);
+bool kernel_cache_enabled();
 
 // Launch over `stripes` stripes of S-byte blocks.  ptrs/strides: n_slots entries.
 int launch_kernel(const Kernel &k, const uint64_t *ptrs, const uint64_t *strides, size_t S, size_t stripes,

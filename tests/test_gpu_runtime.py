@@ -291,3 +291,42 @@ def test_batch_runs_promoted_patterns_on_their_generated_kernels():
                 assert bool((dec[t, keep] == 0xA5).all()), (policy, t)
     finally:
         st.close()
+
+
+def test_auto_promotion_of_a_hot_pattern(tmp_path, monkeypatch):
+    # AUTO: a pattern past the promotion threshold is compiled in a host thread while its calls keep
+    # running on the runtime kernel; a later call loads the generated kernel (bit-exact either way)
+    monkeypatch.setenv("PMRC_KCACHE", str(tmp_path))        # empty cache: the promotion compiles
+    k, n, S, stripes = 4, 8, 64 * 1024, 2
+    st = Stripes(pm.PMRC_MSR_SPARSE, k, n, S, stripes, seed=23)
+    try:
+        st.encode()
+        assert np.array_equal(st.parity.cpu().numpy(), O.encode(O.MSR_SPARSE, n, k, st.d, st.host_data()))
+        pm.pmrc_set_auto_promotion(st.code, 1 << 20)       # 1 MiB of plan traffic
+        f, H = 7, [0, 1, 2, 3, 4, 5]
+        cold = (5, [0, 1, 2, 3, 4, 6])
+        assert pm.pmrc_plan_state(st.code, 1, f, H) == pm.PLAN_RUNTIME_ONLY
+        out = torch.zeros((stripes, st.alpha, S), dtype=torch.uint8, device=DEV)
+        states = []
+        t0 = time.time()
+        while True:
+            out.zero_()
+            pm.pmrc_repair(st.code, f, list(reversed(H)), [st.piece(i) for i in reversed(H)],
+                           (out.data_ptr(), st.alpha * S), S, stripes, st.stream)
+            torch.cuda.synchronize()
+            assert torch.equal(out, st.piece_tensor(f)), states
+            states.append(pm.pmrc_plan_state(st.code, 1, f, H))
+            if states[-1] == pm.PLAN_LOADED or time.time() - t0 > 300:
+                break
+            time.sleep(0.05)
+        assert states[0] in (pm.PLAN_COMPILING, pm.PLAN_COMPILED), states   # promoted after the first call
+        assert states[-1] == pm.PLAN_LOADED, states
+        # a pattern below the threshold stays on the runtime kernel
+        pm.pmrc_set_auto_promotion(st.code, 1 << 40)
+        pm.pmrc_repair(st.code, cold[0], cold[1], [st.piece(i) for i in cold[1]], (out.data_ptr(), st.alpha * S), S,
+                       stripes, st.stream)
+        torch.cuda.synchronize()
+        assert torch.equal(out, st.piece_tensor(cold[0]))
+        assert pm.pmrc_plan_state(st.code, 1, cold[0], cold[1]) == pm.PLAN_RUNTIME_ONLY
+    finally:
+        st.close()

@@ -446,8 +446,20 @@ def main():
                 pm.pmrc_apply(j.code, G[j.k * j.alpha:], Z.data_ptr(), j.B * S, par.data_ptr(), j.P * S, S, j.stripes,
                               st)
             precode()
+            nonsys()
             torch.cuda.synchronize()
             ok = bool(torch.equal(par, j.par))
+            # the non-systematic encode Y = G Z (data taken as the message Z) against the oracle's
+            # product-matrix encoder C = Psi M(Z) (a different code path), sampled stripes
+            import numpy as np
+            import oracle as O
+            okind = {MSR: O.MSR_SPARSE, VAN: O.MSR_VANILLA}[kind]
+            ok_ns = True
+            for t in sorted({0, j.stripes - 1, j.stripes // 2}):
+                p0 = (t * 7919 * 16) % (S - 4096 + 16)
+                z = j.data[t, :, p0:p0 + 4096].cpu().numpy()
+                ok_ns &= bool(np.array_equal(Y[t, :, p0:p0 + 4096].cpu().numpy(),
+                                             O.encode_specific(okind, j.n, j.k, j.d, z)))
             src = j.stripes * j.B * S
             for name, fn, mats in (("encode_nonsystematic", nonsys, [G]), ("precode_then_encode", precode,
                                                                              [Gti, G[j.k * j.alpha:]])):
@@ -455,7 +467,7 @@ def main():
                 naive = sum(pm.pmrc_apply_stats(j.code, m)["naive_lop3"] for m in mats)
                 emit({"op": name, "config": "next2", "kind": KIND_NAMES[kind], "k": 8, "n": 16, "S": S,
                       "ms": round(ms, 4), "GBps": round(src / ms / 1e6, 1), "naive_lop3_per_32pos": naive,
-                      "bit_exact": ok if name == "precode_then_encode" else None})
+                      "bit_exact": ok if name == "precode_then_encode" else ok_ns})
             j.close()
     if "5" in cfgs:
         # BASELINE.json config 5: 64 GiB per point over 8 GPUs = args.gib (8) GiB per GPU; this

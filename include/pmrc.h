@@ -163,8 +163,9 @@ int pmrc_apply(pmrc_code *c, const uint8_t *A, int rows, int cols, const void *i
  *                      coefficients as data): a new pattern costs only the host inversion and a
  *                      table fill (P:216's per-pattern initialisation, well under a millisecond)
  *   PMRC_PLAN_AUTO     (default) JIT for the encode (built at pmrc_create) and for plans whose JIT
- *                      kernel is already loaded on the handle (pmrc_plan_prepare, or a call made
- *                      under PMRC_PLAN_JIT); the runtime kernel for every other GF(2^8) plan.
+ *                      kernel is already loaded on the handle (pmrc_plan_prepare, a call made
+ *                      under PMRC_PLAN_JIT, or automatic promotion: pmrc_set_auto_promotion); the
+ *                      runtime kernel for every other GF(2^8) plan.
  * GF(2^16) codes always use JIT.  Results are bit-identical under every policy. */
 enum { PMRC_PLAN_AUTO = 0, PMRC_PLAN_JIT = 1, PMRC_PLAN_RUNTIME = 2 };
 int pmrc_set_plan_policy(pmrc_code *c, int policy);

@@ -947,8 +947,8 @@ static int repair_spec(const pmrc_code *c, int f, const int *H, int nh, const in
 //   RUNTIME  the precompiled runtime-coefficient kernel (csrc/rt/rlc.cu): coefficients are data,
 //            a new pattern costs the host inversion + table fill (P:216's initialisation)
 // Policy PMRC_PLAN_AUTO (default): JIT for the encode (compiled at pmrc_create) and for plans whose
-// JIT kernel is already loaded on the handle (pmrc_plan_prepare / earlier JIT calls), RUNTIME for
-// every other plan; GF(2^16) plans always use JIT.
+// JIT kernel is already loaded on the handle (pmrc_plan_prepare / earlier JIT calls / a finished
+// background promotion, maybe_promote), RUNTIME for every other plan; GF(2^16) plans always use JIT.
 // ---------------------------------------------------------------------------------------------
 static bool use_runtime(const pmrc_code *c, const std::string &key) {
   if (c->w != 8) return false;

@@ -182,7 +182,7 @@ int pmrc_plan_prepare(pmrc_code *c, int op, int lost_id, const int *ids, int n_i
  * keep running on the runtime kernel; the first call after that loads the cubin (milliseconds) and
  * the pattern runs its generated kernel from then on.  Default 1 GiB; 0 disables.  Needs the kernel
  * cache (PMRC_KCACHE not "off").  Batch calls use promoted patterns but do not count traffic.
- * pmrc_destroy waits for compilations in flight. */
+ * pmrc_destroy waits for compilations in flight (so that no library thread outlives the handle). */
 int pmrc_set_auto_promotion(pmrc_code *c, unsigned long long bytes);
 /* Engine state of a decode (op 0) / repair (op 1) pattern on this handle: 0 runtime kernel (no
  * generated kernel loaded), 1 promotion compiling, 2 promotion compiled (loaded by the next call),

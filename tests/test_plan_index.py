@@ -53,3 +53,21 @@ def test_plan_index_key_follows_generator_options(tmp_path, monkeypatch):
     finally:
         pm.pmrc_destroy(code)
         pm.pmrc_destroy(code2)
+
+
+def test_promotion_controls_without_a_gpu():
+    # the AUTO promotion knobs are host state: a pattern never run is on the runtime kernel (0),
+    # bad ops are EINVAL, and the threshold accepts any 64-bit value (0 = off)
+    code = pm.pmrc_create(pm.PMRC_MSR_SPARSE, 3, 4, 6)
+    try:
+        assert pm.pmrc_plan_state(code, 0, 0, [0, 1, 5]) == pm.PLAN_RUNTIME_ONLY
+        assert pm.pmrc_plan_state(code, 1, 5, [0, 1, 2, 3]) == pm.PLAN_RUNTIME_ONLY
+        for v in (0, 1, 1 << 30, 2 ** 64 - 1):
+            pm.pmrc_set_auto_promotion(code, v)
+        try:
+            pm.pmrc_plan_state(code, 2, 0, [0, 1, 2])
+            raise AssertionError("op 2 accepted")
+        except pm.PmrcError as e:
+            assert e.rc == pm.PMRC_EINVAL
+    finally:
+        pm.pmrc_destroy(code)

@@ -754,7 +754,13 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
 
   const int M = std::max(1, o.chunk_loop);
   // stage-buffer ring per team: NB buffers, prefetch distance D = NB - 1 stages (layouts 1/2)
-  const int NB = (o.layout == 0 || (o.ws && o.team >= 2)) ? 2 : std::max(2, o.nbuf);
+  // The dynamic chunk schedule knows a team's next item one item ahead, so with it the prefetch
+  // distance may not reach past the next item: every group must have >= D stages (else 2 buffers).
+  int min_ns = 1 << 30;
+  for (auto &gs : gstages)
+    if (!gs.empty()) min_ns = std::min(min_ns, (int)gs.size());
+  int NB = (o.layout == 0 || (o.ws && o.team >= 2)) ? 2 : std::max(2, o.nbuf);
+  if (NB > 2 && o.dyn > 0 && o.layout == 1 && NB - 1 > min_ns) NB = 2;
   const int D = NB - 1;
   const int T = std::max(1, o.team);  // warps sharing one chunk's stage buffer
   // warp-specialised teams (o.ws, layouts 1/2): rank 0 loads and transposes every block of a
@@ -917,7 +923,7 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
   const int TPB = 32 * std::max(T, o.warps);
   const int teams = TPB / 32 / T;
   // dynamic chunk schedule (layout 1): teams take their next chunk from a per-group counter
-  const bool DYN = o.dyn > 0 && o.layout == 1 && !WS && NB == 2 && o.pace_lag == 0 && o.cta_sync == 0;
+  const bool DYN = o.dyn > 0 && o.layout == 1 && !WS && o.pace_lag == 0 && o.cta_sync == 0;
   const bool HYB = DYN && o.dyn >= 2 && groups.size() > 1 && o.dyn_static > 0;  // static ranges + pool
   // layout 0 with dynamic tiles: a CTA takes its next tile of teams x chunk_loop chunks from a counter
   const bool DYN0 = o.dyn > 0 && o.layout == 0 && o.sync_groups;
@@ -1357,12 +1363,15 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
         s << "    }\n";
       } else
         s << "    const u32 tau = r * teams + team;\n";
-      if (!gstages[g].empty()) {
-        s << "    if (tau < total) {\n";
-        emit_issue(s, gstages[g][0], "tau", "true", "0u", "      ");
-        s << "    }\n";
+      // the first D stages of the first item (D <= the group's stage count, see NB)
+      for (int pp = 0; pp < D; pp++) {
+        if (pp < (int)gstages[g].size()) {
+          s << "    if (tau < total) {\n";
+          emit_issue(s, gstages[g][pp], "tau", "true", std::to_string(pp) + "u", "      ");
+          s << "    }\n";
+        }
+        s << "    pm_cp_commit();\n";
       }
-      s << "    pm_cp_commit();\n";
     } else {
       const int ns = (int)gstages[g].size();
       for (int pp = 0; pp < D; pp++) {

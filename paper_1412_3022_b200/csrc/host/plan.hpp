@@ -91,6 +91,7 @@ struct GenOptions {
   bool l0_sync = false;     // layout 0: CTA barrier after every chunk of a group visit (teams fetch
                             // the group's code together)
   int rt_groups = 0;        // runtime-coefficient kernel (rtplan.hpp): row groups per CTA (0 = auto)
+  int rt_rows = 0;          // runtime-coefficient kernel: rows per thread, 7 or 8 (0 = auto)
 };
 
 constexpr int kDynSlots = 64;  // counter slots of the dynamic schedule (launches in flight per plan)

@@ -24,10 +24,18 @@ pmrc_rt::RlcShape rt_shape(int n_out, const GenOptions &o) {
   //   V = 2 with 3 or 7 groups -- twice the per-word overhead; 16 rows x 2 words in one group,
   //   which saves the second group's selectors: config-4 decode 2.58 -> 2.85 ms, repair 0.94 -> 1.37)
   // (rt_groups overrides for experiments; tg is set per launch from the plans)
-  pmrc_rt::RlcShape sh = n_out <= 8 ? pmrc_rt::RlcShape{8, 4, 1, 256, false} : pmrc_rt::RlcShape{8, 4, 2, 256, false};
-  if (o.rt_groups == 1) sh = {8, 4, 1, 256, false};
-  if (o.rt_groups == 2) sh = {8, 4, 2, 256, false};
-  return sh;
+  //   R = 7 or 8: the one with fewer passes, then fewer row slots (rows past n_out of a short last
+  //   row block are computed and never stored); ties keep 8 (the k = 8 sparse-MSR encode's 8-row
+  //   symbol groups fill 8-row blocks).  MSR k = 8 repair (7 rows) and config-4 decodes of 4
+  //   missing nodes (28 rows) take R = 7.
+  const int G = o.rt_groups == 1 || o.rt_groups == 2 ? o.rt_groups : (n_out <= 8 ? 1 : 2);
+  auto cost = [&](int R) {
+    const int blocks = (std::max(1, n_out) + R - 1) / R, passes = (blocks + G - 1) / G;
+    return std::make_pair(passes, blocks * R);
+  };
+  int R = cost(7) < cost(8) ? 7 : 8;
+  if (o.rt_rows == 7 || o.rt_rows == 8) R = o.rt_rows;
+  return pmrc_rt::RlcShape{R, 4, G, 256, false};
 }
 
 // PRMT tables of coefficient c (rlc.cu): T0[j] = c*j, T1[j] = c*(j<<3) (j < 8), T2[j] = c*(j<<6) (j < 4),

@@ -448,7 +448,9 @@ static int occ_one(unsigned max_words) {
 }
 
 // the instantiated shapes (rlc.hpp)
-#define RLC_SHAPES(X) X(8, 4, 1, 256, false) X(8, 4, 2, 256, false) X(8, 4, 1, 256, true) X(8, 4, 2, 256, true)
+#define RLC_SHAPES(X)                                                                                \
+  X(8, 4, 1, 256, false) X(8, 4, 2, 256, false) X(8, 4, 1, 256, true) X(8, 4, 2, 256, true)          \
+  X(7, 4, 1, 256, false) X(7, 4, 2, 256, false) X(7, 4, 1, 256, true) X(7, 4, 2, 256, true)
 
 int rlc_launch(const RlcArgs &a, const RlcShape &sh, int grid, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;

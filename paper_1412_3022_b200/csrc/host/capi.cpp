@@ -269,7 +269,6 @@ int apply_gen_knobs(const std::string &s, GenOptions &G, std::string &err) {
       {"grid_ctas", 1, [](GenOptions &o, int v) { o.grid_ctas = v; }},
       {"rt_groups", 0, [](GenOptions &o, int v) { o.rt_groups = v; }},
       {"rt_rows", 0, [](GenOptions &o, int v) { o.rt_rows = v; }},
-      {"l0_sync", 0, [](GenOptions &o, int v) { o.l0_sync = v != 0; }},
   };
   std::string applied;
   size_t pos = 0;

@@ -1232,14 +1232,7 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
       if (!gstages[g2].empty()) { next_g = (int)g2; break; }
     if (o.sync_groups) s << "    __syncthreads();\n";
     s << "    #pragma unroll 1\n";
-    if (o.l0_sync) {
-      // every team runs mt iterations (idle ones skip the work) and the CTA re-aligns after each
-      // chunk, so the teams stream the group's network code together (instruction cache)
-      s << "    for (u32 m = 0; m < mt; m++) {\n";
-      s << "      if (m < cnt) {\n";
-    } else {
-      s << "    for (u32 m = 0; m < cnt; m++) {\n";
-    }
+    s << "    for (u32 m = 0; m < cnt; m++) {\n";
     s << "      const u32 gi = tb + m;\n";
     s << "      const u64 t = pm_udiv(gi, dv_m, dv_s1, dv_s2);\n";
     s << "      const u32 q = gi - (u32)t * chunks;\n";
@@ -1267,7 +1260,6 @@ static __device__ __forceinline__ void pm_tr16(u32 *w) {
       }
       s << "          }\n";
     });
-    if (o.l0_sync) s << "      }\n      __syncthreads();\n";
     s << "    }\n";
   }
   if (DYN0) {

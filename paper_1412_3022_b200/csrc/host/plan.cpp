@@ -70,9 +70,9 @@ static const char kBuildId[] = __DATE__ " " __TIME__;
   X(dyn_static) X(cta_sync) X(chunk_loop) X(team) X(ld_hint) X(fold) X(layout) X(grid_ctas) X(tr_balance)       \
   X(balance_ranks) X(cluster_wide) X(even_groups) X(auto_wide16) X(auto_wide) X(enc_restarts) X(cse_restarts)   \
   X(sched) X(l2_shared) X(ws_prod) X(ws) X(own_first) X(nbuf) X(tr_unroll) X(fence) X(net_even) X(net_in)       \
-  X(trace) X(pace_lag) X(l0_sync) X(rt_groups) X(rt_rows)
+  X(trace) X(pace_lag) X(rt_groups) X(rt_rows)
 #define PMRC_COUNT(m) +1
-static_assert(0 PMRC_GEN_FIELDS(PMRC_COUNT) == 41 && sizeof(GenOptions) == 136,
+static_assert(0 PMRC_GEN_FIELDS(PMRC_COUNT) == 40 && sizeof(GenOptions) == 132,
               "GenOptions changed: list every field in PMRC_GEN_FIELDS (the plan index key)");
 #undef PMRC_COUNT
 

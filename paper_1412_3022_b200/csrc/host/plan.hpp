@@ -88,8 +88,6 @@ struct GenOptions {
   int net_in = 7;           // inputs per CSE sub-network within a stage (0 = the whole stage)
   bool trace = false;       // layout 1 diagnostics: per-team start/end/wait times (pmrc_debug_counters)
   int pace_lag = 0;         // layout 1: max chunks a team runs ahead of its peers (0 = no pacing)
-  bool l0_sync = false;     // layout 0: CTA barrier after every chunk of a group visit (teams fetch
-                            // the group's code together)
   int rt_groups = 0;        // runtime-coefficient kernel (rtplan.hpp): row groups per CTA (0 = auto)
   int rt_rows = 0;          // runtime-coefficient kernel: rows per thread, 7 or 8 (0 = auto)
 };

@@ -164,3 +164,23 @@ def test_rt_decode_blob_k16_tables_in_device_memory():
         assert np.array_equal(out, x)
     finally:
         pm.pmrc_destroy(code)
+
+
+def test_rt_rows_per_thread_follow_the_plan_size():
+    # rows per thread: 7 or 8, the one with fewer passes and then fewer row slots (rtplan.cpp
+    # rt_shape): MSR k = 8 repairs (7 rows) and 4-missing-node decodes (28 rows) take 7, the
+    # 56-row encode (8-row symbol groups) and a 15-row MBR decode keep 8
+    code = pm.pmrc_create(0, 8, 14, 16)
+    mbr = pm.pmrc_create(2, 8, 14, 16)
+    try:
+        def shape(c, op, lost=0, ids=()):
+            h = dict(zip(HDR, [int(v) for v in pm.pmrc_rt_plan_blob(c, op, lost, ids)[:len(HDR)]]))
+            return h["n_out"], h["R"], h["G"], h["n_pass"]
+        assert shape(code, 1, 15, list(range(14))) == (7, 7, 1, 1)
+        assert shape(code, 1, 3, [i for i in range(15) if i != 3]) == (7, 7, 1, 1)
+        assert shape(code, 0, 0, [0, 1, 4, 5, 9, 12, 14, 15]) == (28, 7, 2, 2)
+        assert shape(code, 2) == (56, 8, 2, 4)
+        assert shape(mbr, 0, 0, [0, 1, 4, 5, 6, 7, 11, 14]) == (15, 8, 2, 1)
+    finally:
+        pm.pmrc_destroy(code)
+        pm.pmrc_destroy(mbr)

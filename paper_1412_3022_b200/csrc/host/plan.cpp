@@ -199,13 +199,15 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
       if (oo.warps <= 0) oo.warps = 16;
     } else if (o.auto_wide16 && p.w != 16 && !w0.clustered && w0.max_support_rows >= 16 && w0.groups > 16 &&
                oo.team == 2 && oo.max_rows == 8 && oo.layout < 0) {
-      // many groups whose supports have >= 16 rows (k = 16 encode: 30 groups of 8 rows, two per
-      // support): pairs of them as 16-row groups on 4-warp teams halve the input transposes; layout 0
-      // (measured: MSR k=16 869 -> 901 GB/s; layout 1 with these groups 606)
-      oo.max_rows = 16;
-      oo.team = 4;
-      oo.layout = 0;
-      if (oo.warps <= 0) oo.warps = 16;
+      // many groups whose supports have >= 16 rows (k = 16 encode: 30 / 60 groups of 8 rows, two per
+      // support): group-specialised CTAs (8-row groups on 2-warp teams) with the stealing schedule
+      // (dyn = 2 below: the 148 % G SMs left over visit other groups), so every SM streams one
+      // group's network code for all its chunks.  Measured at config 5's 8 GiB per GPU against the
+      // previous default (16-row groups on 4-warp teams walking all groups in layout 0, which had
+      // beaten layout 0 with 8-row groups: 869 -> 901 GB/s at 1 GiB): MSR k=16 843-858 -> 883 GB/s,
+      // MBR k=16 726-771 -> 868-870 (profiles/r02/k16_layout.jsonl); 16-row groups in layout 1
+      // measure 782 / 670.
+      oo.layout = 1;
     }
   }
   if (oo.dyn < 0) {

@@ -71,8 +71,8 @@ struct GenOptions {
                              // different groups; measured 0.651 -> 0.734 ms: the groups' fronts drift
                              // apart and the shared inputs are read from DRAM twice)
   bool even_groups = false; // clustered plans: equal group sizes instead of max_rows-sized groups
-  bool auto_wide16 = true;   // resolve_options: 16-row groups on 4-warp teams, layout 0, for many
-                             // groups whose supports have >= 16 rows (k = 16 encode)
+  bool auto_wide16 = true;   // resolve_options: group-specialised CTAs (layout 1, stealing schedule)
+                             // for many groups whose supports have >= 16 rows (k = 16 encode)
   bool auto_wide = true;    // resolve_options: 16-row groups on 4-warp teams for wide multi-stage plans
   int enc_restarts = 4;     // CSE restarts for the encode plan (built once per code; capi.cpp)
   int cse_restarts = 1;     // CSE runs per network (seeded near-tie randomisation), keep the cheapest

@@ -141,7 +141,8 @@ def test_plan_stats_and_source_without_gpu():
 
 def test_tuned_plan_shapes_without_gpu():
     # the measured defaults: 16 warps per CTA, static ranges for the sparse encode,
-    # 16-row groups in layout 0 for k = 16, the stealing counters for GF(2^16) k = 8 (14 groups)
+    # group-specialised 8-row groups with the stealing counters for k = 16, and the stealing
+    # counters for GF(2^16) k = 8 (14 groups)
     c = pm.pmrc_create(pm.PMRC_MSR_SPARSE, 8, 14, 16)
     try:
         src = pm.pmrc_encode_source(c)
@@ -152,8 +153,8 @@ def test_tuned_plan_shapes_without_gpu():
     c = pm.pmrc_create(pm.PMRC_MSR_SPARSE, 16, 30, 32)
     try:
         st = pm.pmrc_plan_stats(c, 2)
-        assert st["groups"] == 15                                  # 16-row groups (auto_wide16)
-        assert "per_cta" in pm.pmrc_encode_source(c)               # layout 0
+        assert st["groups"] == 30                                  # 8-row groups (auto_wide16)
+        assert "for (u32 hop = 0; hop < 30u; hop++)" in pm.pmrc_encode_source(c)   # layout 1, dyn 2
     finally:
         pm.pmrc_destroy(c)
     c = pm.pmrc_create(pm.PMRC_MSR_SPARSE, 8, 14, 16, 16)

@@ -134,10 +134,11 @@ int get_kernel(pmrc_code *c, const std::string &key, const PlanSpec &spec, Kerne
 }
 
 // the encode plan is built once per code: CSE restarts with randomised near-ties (keep the cheapest
-// network) are worth their host time there (config 2: 12,362 -> 12,305 XORs, 0.501 -> 0.491 ms)
+// network) are worth their host time there (config 2: 12,362 -> 12,305 XORs, 0.501 -> 0.491 ms;
+// k = 16 at config 5's size: MSR 935 -> 950 GB/s, MBR 882 -> 909, for ~1-3 s more of host time)
 GenOptions enc_gen(const pmrc_code *c) {
   GenOptions g = c->gen;
-  if (c->w == 8 && c->def.k <= 8) g.cse_restarts = std::max(g.cse_restarts, g.enc_restarts);  // (k=16: minutes)
+  if (c->w == 8) g.cse_restarts = std::max(g.cse_restarts, g.enc_restarts);
   return g;
 }
 

@@ -206,8 +206,11 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
       // previous default (16-row groups on 4-warp teams walking all groups in layout 0, which had
       // beaten layout 0 with 8-row groups: 869 -> 901 GB/s at 1 GiB): MSR k=16 843-858 -> 883 GB/s,
       // MBR k=16 726-771 -> 868-870 (profiles/r02/k16_layout.jsonl); 16-row groups in layout 1
-      // measure 782 / 670.
+      // measure 782 / 670.  Stages of <= 10 blocks (30 inputs: 3 x 10, 16 inputs: 2 x 8) fit 16 warps
+      // in the shared-memory budget where 15-block stages fit 14: MSR 884 -> 935 GB/s, MBR 867 -> 882
+      // (with the encode's best-of-4 CSE, capi.cpp: 950 / 909; profiles/r02/k16_knobs.jsonl)
       oo.layout = 1;
+      if (oo.in_block == 16) oo.in_block = 10;
     }
   }
   if (oo.dyn < 0) {

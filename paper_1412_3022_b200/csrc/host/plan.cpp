@@ -197,6 +197,16 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
       oo.max_rows = 16;
       oo.team = 4;
       if (oo.warps <= 0) oo.warps = 16;
+      if (p.outputs.size() <= 16 && oo.warps == 16 && oo.in_block == 16 && o.warps <= 0) {
+        // a single group of 9-16 rows (two missing systematic nodes): 8 rows per warp on 2-warp
+        // teams, 8 warps, stages of <= 21 blocks -- half the warps meeting at each team barrier and
+        // fewer barriers per chunk: MBR decodes of 15 missing blocks 0.252 -> 0.220 ms (config 3's
+        // survivors), MSR of 14 0.302 -> 0.288; plans of 1 or >= 3 missing nodes measured slower
+        // this way and keep their shapes (profiles/r02/decode_shapes.jsonl)
+        oo.team = 2;
+        oo.warps = 8;
+        oo.in_block = 21;
+      }
     } else if (o.auto_wide16 && p.w != 16 && !w0.clustered && w0.max_support_rows >= 16 && w0.groups > 16 &&
                oo.team == 2 && oo.max_rows == 8 && oo.layout < 0) {
       // many groups whose supports have >= 16 rows (k = 16 encode: 30 / 60 groups of 8 rows, two per

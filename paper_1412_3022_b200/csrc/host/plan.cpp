@@ -197,16 +197,6 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
       oo.max_rows = 16;
       oo.team = 4;
       if (oo.warps <= 0) oo.warps = 16;
-      if (p.outputs.size() <= 16 && oo.warps == 16 && oo.in_block == 16 && o.warps <= 0) {
-        // a single group of 9-16 rows (two missing systematic nodes): 8 rows per warp on 2-warp
-        // teams, 8 warps, stages of <= 21 blocks -- half the warps meeting at each team barrier and
-        // fewer barriers per chunk: MBR decodes of 15 missing blocks 0.252 -> 0.220 ms (config 3's
-        // survivors), MSR of 14 0.302 -> 0.288; plans of 1 or >= 3 missing nodes measured slower
-        // this way and keep their shapes (profiles/r02/decode_shapes.jsonl)
-        oo.team = 2;
-        oo.warps = 8;
-        oo.in_block = 21;
-      }
     } else if (o.auto_wide16 && p.w != 16 && !w0.clustered && w0.max_support_rows >= 16 && w0.groups > 16 &&
                oo.team == 2 && oo.max_rows == 8 && oo.layout < 0) {
       // many groups whose supports have >= 16 rows (k = 16 encode: 30 / 60 groups of 8 rows, two per
@@ -221,6 +211,22 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
       // (with the encode's best-of-4 CSE, capi.cpp: 950 / 909; profiles/r02/k16_knobs.jsonl)
       oo.layout = 1;
       if (oo.in_block == 16) oo.in_block = 10;
+    }
+    // One group of 9-16 rows -- decode rows clustered into a single group (two missing systematic
+    // nodes), or rows sharing one support (the fused repair of an MBR node: alpha = d = 14 rows,
+    // which 8-row groups split in two, each re-reading every helper block): 8 rows per warp on
+    // 2-warp teams, 8 warps (half the warps meeting at each team barrier), and a 3-deep stage ring
+    // when the group has >= 3 stages.  Measured (profiles/r02/decode_shapes.jsonl,
+    // repair_shapes.jsonl): config-3 MBR decode 0.252 -> 0.222 ms, MSR decode of 14 rows 0.302 ->
+    // 0.275, MBR repair of a parity node 0.562 -> 0.454-0.460, of a systematic node 0.089 -> 0.076;
+    // 7-row MSR repairs (<= 8 rows) and decodes of > 16 rows keep their shapes (slower this way)
+    const size_t nout = p.outputs.size();
+    if (p.w != 16 && nout > 8 && nout <= 16 && (w0.clustered || w0.max_support_rows >= (int)nout) &&
+        o.team == 2 && o.max_rows == 8 && o.warps <= 0 && o.nbuf == 2 && o.in_block == 16) {
+      oo.max_rows = 16;
+      oo.team = 2;
+      oo.warps = 8;
+      if (w0.max_stages >= 3) oo.nbuf = 3;
     }
   }
   if (oo.dyn < 0) {

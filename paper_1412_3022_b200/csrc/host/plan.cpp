@@ -219,14 +219,30 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     // when the group has >= 3 stages.  Measured (profiles/r02/decode_shapes.jsonl,
     // repair_shapes.jsonl): config-3 MBR decode 0.252 -> 0.222 ms, MSR decode of 14 rows 0.302 ->
     // 0.275, MBR repair of a parity node 0.562 -> 0.454-0.460, of a systematic node 0.089 -> 0.076;
-    // 7-row MSR repairs (<= 8 rows) and decodes of > 16 rows keep their shapes (slower this way)
+    // 7-row MSR repairs (<= 8 rows) and decodes of > 16 rows keep their shapes (slower this way).
+    // ALU-heavy plans (decodes) run 12 warps (6 teams; 158-164 registers fit the 170 of 384 threads,
+    // so the stage ring stays 2 deep in the shared-memory budget) with sub-networks of 8 inputs (16-
+    // block stages as 8 + 8 instead of 6 + 5 + 5: -7.5% XORs, no spills): ncu of the 8-warp shape
+    // showed nothing saturated (ALU 60%, shared memory 39%, DRAM 49%) and fixed-latency `wait`
+    // stalls on top with 2 warps per SMSP.  Measured (profiles/r02/dec3_shapes.txt): config-3 MBR
+    // decode 0.221 -> 0.204 ms, MSR 14-row decode 0.277 -> 0.246; the MBR fused repair keeps 8
+    // warps and the 3-deep ring (0.459 vs 0.493 ms with 12 warps)
     const size_t nout = p.outputs.size();
     if (p.w != 16 && nout > 8 && nout <= 16 && (w0.clustered || w0.max_support_rows >= (int)nout) &&
         o.team == 2 && o.max_rows == 8 && o.warps <= 0 && o.nbuf == 2 && o.in_block == 16) {
       oo.max_rows = 16;
       oo.team = 2;
-      oo.warps = 8;
-      if (w0.max_stages >= 3) oo.nbuf = 3;
+      // ALU-heavy plans (>= 40 naive LOP3 per 32 positions of each block read or written: these
+      // decodes 62-79; the MBR parity-node repair, 196 helper blocks, 19) take the 12-warp shape
+      long blocks = (long)nout;
+      for (const auto &in : p.inputs) blocks += (long)in.terms.size();
+      if (w0.naive_lop3 >= 40L * blocks) {
+        oo.warps = 12;
+        if (o.net_in == 7) oo.net_in = 8;
+      } else {
+        oo.warps = 8;
+        if (w0.max_stages >= 3) oo.nbuf = 3;
+      }
     }
   }
   if (oo.dyn < 0) {

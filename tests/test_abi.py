@@ -162,6 +162,17 @@ def test_tuned_plan_shapes_without_gpu():
         assert "for (u32 hop = 0; hop < 14u; hop++)" in pm.pmrc_encode_source(c)
     finally:
         pm.pmrc_destroy(c)
+    # one group of 9-16 rows: decodes (clustered rows) on 12 warps with 8-input sub-networks, the
+    # MBR fused repair (one shared support) on 8 warps
+    c = pm.pmrc_create(pm.PMRC_MBR, 8, 14, 16)
+    try:
+        dec = pm.pmrc_plan_source(c, 0, 0, [0, 1, 4, 5, 6, 7, 11, 14])
+        assert "__launch_bounds__(384, 1)" in dec
+        assert pm.pmrc_plan_stats(c, 0, 0, [0, 1, 4, 5, 6, 7, 11, 14])["xor2"] <= 6927
+        rep = pm.pmrc_plan_source(c, 1, 15, list(range(14)))
+        assert "__launch_bounds__(256, 1)" in rep
+    finally:
+        pm.pmrc_destroy(c)
 
 
 def test_independent_launches_flag_without_gpu():

@@ -22,9 +22,11 @@
 //     LOP3 mux + IMAD shifts) into 8 bit planes; the XOR network reads planes with LDS.128, keeps
 //     the group's 8 x 8 output planes in registers, then transposes back and stores 16-B vectors.
 #include <algorithm>
+#include <atomic>
 #include <functional>
 #include <map>
 #include <sstream>
+#include <thread>
 
 #include "plan.hpp"
 
@@ -528,6 +530,95 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
       mx = std::max(mx, c);
     }
     st.group_cost_ratio = groups.empty() ? 1.0 : (double)mx / (double)std::max(1L, mn);
+  }
+  // ---- partition search (part_search != 0): a single-stage group of plain inputs is computed as
+  // T ranks (row shares) x sub-networks (input shares), each with its own CSE.  Which inputs share
+  // a sub-network and which rows share a warp is free: hill-climb over swaps of two inputs between
+  // sub-networks / two rows between ranks, minimising the slower rank's LOP3 count (the ranks meet
+  // at a barrier), then the total.  Deterministic (fixed seeds); the groups search in parallel.
+  // part_search > 0 searches plans of unequal groups only, < 0 every plan.  Measured (200 and 600
+  // evaluations, profiles/r02/part_search.jsonl): MBR k = 8 encode (14- and 8-input groups) 19,960 ->
+  // 19,700 XORs, 0.573 -> 0.559 ms; the MSR k = 8 encode's equal groups lose 1.5% of their XORs
+  // (12,305 -> 12,122) but run 0.8% slower (0.491 -> 0.495 ms), MSR k = 4 is unchanged.
+  if (o.part_search != 0 && (o.part_search < 0 || st.group_cost_ratio > 1.2) && o.cse && W == 8 && !st.clustered &&
+      !(o.ws && o.layout >= 1)) {
+    const int evals = std::abs(o.part_search);
+    const int TT = std::max(1, o.team);
+    auto search = [&](Group &G, uint32_t seed) {
+      int tot = 0;
+      for (int c : G.cols) {
+        if (p.inputs[c].terms.size() != 1) return;
+        tot++;
+      }
+      const int ncols = (int)G.cols.size(), mall = (int)G.rows.size();
+      if (tot > std::max(1, o.in_block)) return;  // more than one stage
+      int sub = o.net_in > 0 ? o.net_in : ncols;
+      if (o.net_even && sub < ncols) {
+        const int nsub = (ncols + sub - 1) / sub;
+        sub = (ncols + nsub - 1) / nsub;
+      }
+      const bool col_moves = sub < ncols, row_moves = TT >= 2 && mall >= 2 * TT;
+      if (!col_moves && !row_moves) return;
+      auto cost = [&](const std::vector<int> &rw, const std::vector<int> &cl) {
+        long worst = 0, total = 0;
+        for (int rk = 0; rk < TT; rk++) {
+          const int r0 = mall * rk / TT, m = mall * (rk + 1) / TT - r0;
+          long mine = 0;
+          for (int c0 = 0; c0 < ncols; c0 += sub) {
+            const int c1 = std::min(ncols, c0 + sub);
+            std::vector<std::vector<int>> sr(W * m);
+            for (int r = 0; r < m; r++)
+              for (int ci = c0; ci < c1; ci++) {
+                const uint32_t cf = p.coef(rw[r0 + r], cl[ci]);
+                if (!cf) continue;
+                uint32_t br[16];
+                coef_rows_w(W, cf, br);
+                for (int b = 0; b < W; b++)
+                  for (int bp = 0; bp < W; bp++)
+                    if ((br[b] >> bp) & 1) sr[r * W + b].push_back((ci - c0) * W + bp);
+              }
+            mine += cse3(W * (c1 - c0), sr, 0).lop3();
+          }
+          worst = std::max(worst, mine);
+          total += mine;
+        }
+        return worst * 100000 + total;
+      };
+      std::vector<int> rw = G.rows, cl = G.cols;
+      long cur = cost(rw, cl);
+      uint32_t x = seed * 2654435761u + 12345u;
+      auto rnd = [&](int n) {
+        x ^= x << 13, x ^= x >> 17, x ^= x << 5;
+        return (int)(x % (uint32_t)n);
+      };
+      for (int it = 0; it < evals; it++) {
+        std::vector<int> r2 = rw, c2 = cl;
+        if (row_moves && (!col_moves || it % 3 == 2)) {
+          const int a = rnd(TT), b = (a + 1 + rnd(TT - 1)) % TT;
+          const int ia = mall * a / TT + rnd(mall * (a + 1) / TT - mall * a / TT);
+          const int ib = mall * b / TT + rnd(mall * (b + 1) / TT - mall * b / TT);
+          std::swap(r2[ia], r2[ib]);
+        } else {
+          const int ia = rnd(ncols);
+          int ib = rnd(ncols);
+          for (int tries = 0; ia / sub == ib / sub && tries < 64; tries++) ib = rnd(ncols);
+          if (ia / sub == ib / sub) continue;
+          std::swap(c2[ia], c2[ib]);
+        }
+        const long c = cost(r2, c2);
+        if (c <= cur) cur = c, rw.swap(r2), cl.swap(c2);
+      }
+      G.rows = rw;
+      G.cols = cl;
+    };
+    std::vector<std::thread> th;
+    const size_t nth = std::min<size_t>(groups.size(), std::max(1u, std::thread::hardware_concurrency()));
+    std::atomic<size_t> next{0};
+    for (size_t t = 0; t < nth; t++)
+      th.emplace_back([&] {
+        for (size_t g = next++; g < groups.size(); g = next++) search(groups[g], (uint32_t)g + 1);
+      });
+    for (auto &t : th) t.join();
   }
 
   // ---- stages: each group's inputs packed into shared-memory buffers of <= IB loaded blocks ----

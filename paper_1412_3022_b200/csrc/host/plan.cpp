@@ -70,9 +70,9 @@ static const char kBuildId[] = __DATE__ " " __TIME__;
   X(dyn_static) X(cta_sync) X(chunk_loop) X(team) X(ld_hint) X(fold) X(layout) X(grid_ctas) X(tr_balance)       \
   X(balance_ranks) X(cluster_wide) X(even_groups) X(auto_wide16) X(auto_wide) X(enc_restarts) X(cse_restarts)   \
   X(sched) X(l2_shared) X(ws_prod) X(ws) X(own_first) X(nbuf) X(tr_unroll) X(fence) X(net_even) X(net_in)       \
-  X(trace) X(pace_lag) X(rt_groups) X(rt_rows)
+  X(trace) X(pace_lag) X(rt_groups) X(rt_rows) X(part_search) X(enc_part_search)
 #define PMRC_COUNT(m) +1
-static_assert(0 PMRC_GEN_FIELDS(PMRC_COUNT) == 40 && sizeof(GenOptions) == 132,
+static_assert(0 PMRC_GEN_FIELDS(PMRC_COUNT) == 42 && sizeof(GenOptions) == 140,
               "GenOptions changed: list every field in PMRC_GEN_FIELDS (the plan index key)");
 #undef PMRC_COUNT
 
@@ -179,6 +179,8 @@ static void probe(const PlanSpec &p, GenOptions o, GenStats &st) {
   o.cse = false;
   o.cse_restarts = 1;
   o.enc_restarts = 1;
+  o.part_search = 0;
+  o.enc_part_search = 0;
   (void)generate_source(p, o, st);
 }
 
@@ -239,9 +241,16 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
       if (w0.naive_lop3 >= 40L * blocks) {
         oo.warps = 12;
         if (o.net_in == 7) oo.net_in = 8;
+      } else if (w0.max_stages >= 3) {
+        // light multi-stage plans (the MBR parity-node repair: 14 stages of one helper's 14 blocks):
+        // with 8 warps and a 3-deep ring the kernel time depends on the helper set -- 0.46 ms when
+        // all k systematic nodes help, 0.70-0.72 ms when one of them is the node left out (8 of the
+        // 15 choices of 14 helpers; no generator knob at 8 warps moves it: fence, net_in, nbuf 4,
+        // static ranges) -- while 12 warps with the 2-deep ring run both at 0.49 ms
+        // (profiles/r02/mbr_repair_patterns*.jsonl)
+        oo.warps = 12;
       } else {
         oo.warps = 8;
-        if (w0.max_stages >= 3) oo.nbuf = 3;
       }
     }
   }

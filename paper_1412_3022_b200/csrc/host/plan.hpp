@@ -90,6 +90,8 @@ struct GenOptions {
   int pace_lag = 0;         // layout 1: max chunks a team runs ahead of its peers (0 = no pacing)
   int rt_groups = 0;        // runtime-coefficient kernel (rtplan.hpp): row groups per CTA (0 = auto)
   int rt_rows = 0;          // runtime-coefficient kernel: rows per thread, 7 or 8 (0 = auto)
+  int part_search = 0;      // evaluations of the input / row partition search per single-stage group (codegen.cpp)
+  int enc_part_search = 200; // part_search of the encode plan (built once per code; capi.cpp)
 };
 
 constexpr int kDynSlots = 64;  // counter slots of the dynamic schedule (launches in flight per plan)

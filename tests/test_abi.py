@@ -163,14 +163,17 @@ def test_tuned_plan_shapes_without_gpu():
     finally:
         pm.pmrc_destroy(c)
     # one group of 9-16 rows: decodes (clustered rows) on 12 warps with 8-input sub-networks, the
-    # MBR fused repair (one shared support) on 8 warps
+    # MBR fused repair (parity node: 14 stages; systematic node: ALU-heavy) on 12 warps too
     c = pm.pmrc_create(pm.PMRC_MBR, 8, 14, 16)
     try:
+        assert pm.pmrc_plan_stats(c, 2)["xor2"] <= 19700          # + the input / row partition search
         dec = pm.pmrc_plan_source(c, 0, 0, [0, 1, 4, 5, 6, 7, 11, 14])
         assert "__launch_bounds__(384, 1)" in dec
         assert pm.pmrc_plan_stats(c, 0, 0, [0, 1, 4, 5, 6, 7, 11, 14])["xor2"] <= 6927
         rep = pm.pmrc_plan_source(c, 1, 15, list(range(14)))
-        assert "__launch_bounds__(256, 1)" in rep
+        assert "__launch_bounds__(384, 1)" in rep
+        rep = pm.pmrc_plan_source(c, 1, 3, [i for i in range(15) if i != 3])
+        assert "__launch_bounds__(384, 1)" in rep                  # systematic node: ALU-heavy class
     finally:
         pm.pmrc_destroy(c)
 

@@ -66,6 +66,19 @@ int main(int argc, char **argv) {
     const long def = cost(rows, cols);
     long best = def, worst = def;
     std::vector<int> rw = rows, cl = cols;
+    if (getenv("HILL")) {
+      // hill climb: swap one input between the two sub-networks or one row between the two warps
+      long cur = def;
+      for (int t = 0; t < trials; t++) {
+        std::vector<int> r2 = rw, c2 = cl;
+        if (t % 3 == 2) std::swap(r2[rng() % 4], r2[4 + rng() % 4]);
+        else std::swap(c2[rng() % 7], c2[7 + rng() % 7]);
+        const long c = cost(r2, c2);
+        if (c <= cur) { cur = c; rw = r2; cl = c2; }
+        worst = std::max(worst, c);
+      }
+      best = cur;
+    } else
     for (int t = 0; t < trials; t++) {
       std::shuffle(cl.begin(), cl.end(), rng);
       if (t & 1) std::shuffle(rw.begin(), rw.end(), rng);

@@ -139,7 +139,7 @@ int get_kernel(pmrc_code *c, const std::string &key, const PlanSpec &spec, Kerne
 GenOptions enc_gen(const pmrc_code *c) {
   GenOptions g = c->gen;
   if (c->w == 8) g.cse_restarts = std::max(g.cse_restarts, g.enc_restarts);
-  if (c->w == 8) g.part_search = std::max(g.part_search, g.enc_part_search);
+  if (c->w == 8 && g.part_search == 0) g.part_search = g.enc_part_search;
   return g;
 }
 
@@ -240,7 +240,7 @@ int apply_gen_knobs(const std::string &s, GenOptions &G, std::string &err) {
       {"cta_sync", 0, [](GenOptions &o, int v) { o.cta_sync = v; }},
       {"dyn", -1, [](GenOptions &o, int v) { o.dyn = v; }},
       {"enc_restarts", 1, [](GenOptions &o, int v) { o.enc_restarts = v; }},
-      {"part_search", 0, [](GenOptions &o, int v) { o.part_search = v; }},
+      {"part_search", -100000, [](GenOptions &o, int v) { o.part_search = v; }},
       {"enc_part_search", 0, [](GenOptions &o, int v) { o.enc_part_search = v; }},
       {"smem_kib", 0, [](GenOptions &o, int v) { o.smem_kib = v; }},
       {"pdl", 0, [](GenOptions &o, int v) { o.pdl = v; }},

@@ -531,8 +531,8 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     }
     st.group_cost_ratio = groups.empty() ? 1.0 : (double)mx / (double)std::max(1L, mn);
   }
-  // ---- partition search (part_search != 0): a single-stage group of plain inputs is computed as
-  // T ranks (row shares) x sub-networks (input shares), each with its own CSE.  Which inputs share
+  // ---- partition search (part_search != 0): a group of plain inputs is computed as T ranks (row
+  // shares) x stages x sub-networks (input shares), each (rank, sub-network) with its own CSE.  Which inputs share
   // a sub-network and which rows share a warp is free: hill-climb over swaps of two inputs between
   // sub-networks / two rows between ranks, minimising the slower rank's LOP3 count (the ranks meet
   // at a barrier), then the total.  Deterministic (fixed seeds); the groups search in parallel.
@@ -545,47 +545,64 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
     const int evals = std::abs(o.part_search);
     const int TT = std::max(1, o.team);
     auto search = [&](Group &G, uint32_t seed) {
-      int tot = 0;
-      for (int c : G.cols) {
+      for (int c : G.cols)
         if (p.inputs[c].terms.size() != 1) return;
-        tot++;
-      }
       const int ncols = (int)G.cols.size(), mall = (int)G.rows.size();
-      if (tot > std::max(1, o.in_block)) return;  // more than one stage
-      int sub = o.net_in > 0 ? o.net_in : ncols;
-      if (o.net_even && sub < ncols) {
-        const int nsub = (ncols + sub - 1) / sub;
-        sub = (ncols + nsub - 1) / nsub;
+      // segments: the stages the inputs are packed into (the rule of the stage loop below), each
+      // cut into sub-networks (the rule of the network emission); seg0[q] = first input of segment q
+      const int IB = std::max(1, o.in_block);
+      int cap = IB;
+      if (o.stage_even) {
+        const int nst = std::max(1, (ncols + IB - 1) / IB);
+        cap = std::min(IB, (ncols + nst - 1) / nst);
       }
-      const bool col_moves = sub < ncols, row_moves = TT >= 2 && mall >= 2 * TT;
+      std::vector<int> seg0;
+      for (int s0 = 0; s0 < ncols; s0 += cap) {
+        const int ncs = std::min(cap, ncols - s0);
+        int sub = o.net_in > 0 ? o.net_in : ncs;
+        if (o.net_even && sub < ncs) {
+          const int nsub = (ncs + sub - 1) / sub;
+          sub = (ncs + nsub - 1) / nsub;
+        }
+        for (int c0 = 0; c0 < ncs; c0 += sub) seg0.push_back(s0 + c0);
+      }
+      const int nseg = (int)seg0.size();
+      seg0.push_back(ncols);
+      std::vector<int> seg_of(ncols);
+      for (int q = 0; q < nseg; q++)
+        for (int ci = seg0[q]; ci < seg0[q + 1]; ci++) seg_of[ci] = q;
+      const bool col_moves = nseg >= 2, row_moves = TT >= 2 && mall >= 2 * TT;
       if (!col_moves && !row_moves) return;
-      auto cost = [&](const std::vector<int> &rw, const std::vector<int> &cl) {
+      auto net = [&](const std::vector<int> &rw, const std::vector<int> &cl, int rk, int q) {
+        const int r0 = mall * rk / TT, m = mall * (rk + 1) / TT - r0, c0 = seg0[q], c1 = seg0[q + 1];
+        std::vector<std::vector<int>> sr(W * m);
+        for (int r = 0; r < m; r++)
+          for (int ci = c0; ci < c1; ci++) {
+            const uint32_t cf = p.coef(rw[r0 + r], cl[ci]);
+            if (!cf) continue;
+            uint32_t br[16];
+            coef_rows_w(W, cf, br);
+            for (int b = 0; b < W; b++)
+              for (int bp = 0; bp < W; bp++)
+                if ((br[b] >> bp) & 1) sr[r * W + b].push_back((ci - c0) * W + bp);
+          }
+        return cse3(W * (c1 - c0), sr, 0).lop3();
+      };
+      auto score = [&](const std::vector<long> &c) {  // c[rk * nseg + q]
         long worst = 0, total = 0;
         for (int rk = 0; rk < TT; rk++) {
-          const int r0 = mall * rk / TT, m = mall * (rk + 1) / TT - r0;
           long mine = 0;
-          for (int c0 = 0; c0 < ncols; c0 += sub) {
-            const int c1 = std::min(ncols, c0 + sub);
-            std::vector<std::vector<int>> sr(W * m);
-            for (int r = 0; r < m; r++)
-              for (int ci = c0; ci < c1; ci++) {
-                const uint32_t cf = p.coef(rw[r0 + r], cl[ci]);
-                if (!cf) continue;
-                uint32_t br[16];
-                coef_rows_w(W, cf, br);
-                for (int b = 0; b < W; b++)
-                  for (int bp = 0; bp < W; bp++)
-                    if ((br[b] >> bp) & 1) sr[r * W + b].push_back((ci - c0) * W + bp);
-              }
-            mine += cse3(W * (c1 - c0), sr, 0).lop3();
-          }
+          for (int q = 0; q < nseg; q++) mine += c[rk * nseg + q];
           worst = std::max(worst, mine);
           total += mine;
         }
-        return worst * 100000 + total;
+        return worst * 1000000 + total;
       };
       std::vector<int> rw = G.rows, cl = G.cols;
-      long cur = cost(rw, cl);
+      std::vector<long> cc(TT * nseg);
+      for (int rk = 0; rk < TT; rk++)
+        for (int q = 0; q < nseg; q++) cc[rk * nseg + q] = net(rw, cl, rk, q);
+      long cur = score(cc);
       uint32_t x = seed * 2654435761u + 12345u;
       auto rnd = [&](int n) {
         x ^= x << 13, x ^= x >> 17, x ^= x << 5;
@@ -593,20 +610,24 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
       };
       for (int it = 0; it < evals; it++) {
         std::vector<int> r2 = rw, c2 = cl;
+        std::vector<long> n2 = cc;
         if (row_moves && (!col_moves || it % 3 == 2)) {
           const int a = rnd(TT), b = (a + 1 + rnd(TT - 1)) % TT;
           const int ia = mall * a / TT + rnd(mall * (a + 1) / TT - mall * a / TT);
           const int ib = mall * b / TT + rnd(mall * (b + 1) / TT - mall * b / TT);
           std::swap(r2[ia], r2[ib]);
+          for (int q = 0; q < nseg; q++) n2[a * nseg + q] = net(r2, c2, a, q), n2[b * nseg + q] = net(r2, c2, b, q);
         } else {
           const int ia = rnd(ncols);
           int ib = rnd(ncols);
-          for (int tries = 0; ia / sub == ib / sub && tries < 64; tries++) ib = rnd(ncols);
-          if (ia / sub == ib / sub) continue;
+          for (int tries = 0; seg_of[ia] == seg_of[ib] && tries < 64; tries++) ib = rnd(ncols);
+          if (seg_of[ia] == seg_of[ib]) continue;
           std::swap(c2[ia], c2[ib]);
+          for (int rk = 0; rk < TT; rk++)
+            for (int q : {seg_of[ia], seg_of[ib]}) n2[rk * nseg + q] = net(r2, c2, rk, q);
         }
-        const long c = cost(r2, c2);
-        if (c <= cur) cur = c, rw.swap(r2), cl.swap(c2);
+        const long c = score(n2);
+        if (c <= cur) cur = c, rw.swap(r2), cl.swap(c2), cc.swap(n2);
       }
       G.rows = rw;
       G.cols = cl;

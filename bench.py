@@ -217,7 +217,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="pmrc", choices=["pmrc", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--sustained-s", type=float, default=1.0, help="seconds of back-to-back launches for the "
                     "'sustained' figure (0 = skip)")
     ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
@@ -366,7 +366,12 @@ def main():
         tmax = pdist.max_over_ranks(sum(times) / len(times), dist if world > 1 else None, device=dev)
         e2e = {"value": pdist.aggregate_gbps(REAL, world, tmax), "unit": "GB/s",
                "h2d_bytes_per_step": stripes * B * S_, "d2h_bytes_per_step": stripes * P * S_,
-               "api": "pmrc_encode_host (pinned host buffers, staged + overlapped copies)"}
+               "api": "pmrc_encode_host (pinned host buffers, staged + overlapped copies)",
+               "steps": len(times), "ms_per_step": 1e3 * sum(times) / len(times),
+               "ms_per_step_median": 1e3 * sorted(times)[len(times) // 2],
+               "note": "value = mean over the steps (host wall clock around the synchronous call); one run on a "
+                       "busy host measured 31 GB/s where the same box gave 44.7 minutes later "
+                       "(pinned-copy ceiling 50 GB/s each way, tools/pcie_bw.py)"}
         del hd, hp
 
     cpu = None

@@ -567,6 +567,10 @@ std::string generate_source(const PlanSpec &p, const GenOptions &o, GenStats &st
         for (int c0 = 0; c0 < ncs; c0 += sub) seg0.push_back(s0 + c0);
       }
       const int nseg = (int)seg0.size();
+      // multi-stage groups (k = 16: 30 inputs in 3 stages) only on request (part_search < 0): the
+      // search shortens their networks by 1.4% but the kernels measure 0.2-0.7% slower
+      // (profiles/r02/part_search_k16.jsonl)
+      if (ncols > cap && o.part_search > 0) return;
       seg0.push_back(ncols);
       std::vector<int> seg_of(ncols);
       for (int q = 0; q < nseg; q++)

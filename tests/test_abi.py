@@ -178,6 +178,32 @@ def test_tuned_plan_shapes_without_gpu():
         pm.pmrc_destroy(c)
 
 
+def test_partition_search_is_deterministic_and_optional(monkeypatch):
+    # encode plans of unequal groups search the input / row partition of their CSE
+    # sub-networks (parallel host threads, fixed seeds): the same source every time, fewer XORs than
+    # the unsearched plan, the same naive count (the matrix is untouched); part_search < 0 searches
+    # every plan, enc_part_search=0 none
+    def stats_and_source(kind, k, d, n):
+        c = pm.pmrc_create(kind, k, d, n)
+        try:
+            return pm.pmrc_plan_stats(c, 2), pm.pmrc_encode_source(c)
+        finally:
+            pm.pmrc_destroy(c)
+    st1, src1 = stats_and_source(pm.PMRC_MBR, 8, 14, 16)
+    st2, src2 = stats_and_source(pm.PMRC_MBR, 8, 14, 16)
+    assert src1 == src2 and st1 == st2
+    monkeypatch.setenv("PMRC_GEN", "enc_part_search=0")
+    st0, src0 = stats_and_source(pm.PMRC_MBR, 8, 14, 16)
+    assert st0["naive_lop3"] == st1["naive_lop3"] and st1["xor2"] < st0["xor2"] and src0 != src1
+    msr0, _ = stats_and_source(pm.PMRC_MSR_SPARSE, 4, 6, 8)
+    monkeypatch.setenv("PMRC_GEN", "part_search=-60")
+    msr1, _ = stats_and_source(pm.PMRC_MSR_SPARSE, 4, 6, 8)      # equal groups: searched only on request
+    assert msr1["xor2"] <= msr0["xor2"] and msr1["naive_lop3"] == msr0["naive_lop3"]
+    monkeypatch.delenv("PMRC_GEN")
+    msr2, _ = stats_and_source(pm.PMRC_MSR_SPARSE, 4, 6, 8)
+    assert msr2 == msr0
+
+
 def test_independent_launches_flag_without_gpu():
     c = pm.pmrc_create(pm.PMRC_MSR_SPARSE, 8, 14, 16)
     try:

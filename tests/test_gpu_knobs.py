@@ -40,3 +40,18 @@ def test_decode_and_repair_with_non_default_shapes(monkeypatch, gen, policy):
             assert torch.equal(piece, st.piece_tensor(f)), f
     finally:
         st.close()
+
+
+@pytest.mark.parametrize("kind,k,n", [(pm.PMRC_MSR_SPARSE, 8, 16), (pm.PMRC_MSR_SPARSE, 16, 32), (pm.PMRC_MBR, 4, 8)])
+def test_encode_with_the_partition_search_on_every_plan(monkeypatch, kind, k, n):
+    # part_search < 0: equal groups and multi-stage groups (k = 16) are searched too; the reordered
+    # inputs / rows must not change a byte
+    monkeypatch.setenv("PMRC_GEN", "part_search=-40")
+    S, stripes = 2048 + 1024 + 16, 2
+    st = Stripes(kind, k, n, S, stripes, seed=43)
+    try:
+        st.encode()
+        assert np.array_equal(st.parity.cpu().numpy(),
+                              O.encode(oracle_kind(st.kind), n, k, st.d, st.host_data()))
+    finally:
+        st.close()

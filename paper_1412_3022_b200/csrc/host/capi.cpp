@@ -242,6 +242,7 @@ int apply_gen_knobs(const std::string &s, GenOptions &G, std::string &err) {
       {"enc_restarts", 1, [](GenOptions &o, int v) { o.enc_restarts = v; }},
       {"part_search", -100000, [](GenOptions &o, int v) { o.part_search = v; }},
       {"enc_part_search", 0, [](GenOptions &o, int v) { o.enc_part_search = v; }},
+      {"auto_nbuf", 0, [](GenOptions &o, int v) { o.auto_nbuf = v != 0; }},
       {"smem_kib", 0, [](GenOptions &o, int v) { o.smem_kib = v; }},
       {"pdl", 0, [](GenOptions &o, int v) { o.pdl = v; }},
       {"auto_wide16", 0, [](GenOptions &o, int v) { o.auto_wide16 = v != 0; }},

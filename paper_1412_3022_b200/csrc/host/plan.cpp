@@ -70,9 +70,9 @@ static const char kBuildId[] = __DATE__ " " __TIME__;
   X(dyn_static) X(cta_sync) X(chunk_loop) X(team) X(ld_hint) X(fold) X(layout) X(grid_ctas) X(tr_balance)       \
   X(balance_ranks) X(cluster_wide) X(even_groups) X(auto_wide16) X(auto_wide) X(enc_restarts) X(cse_restarts)   \
   X(sched) X(l2_shared) X(ws_prod) X(ws) X(own_first) X(nbuf) X(tr_unroll) X(fence) X(net_even) X(net_in)       \
-  X(trace) X(pace_lag) X(rt_groups) X(rt_rows) X(part_search) X(enc_part_search)
+  X(trace) X(pace_lag) X(rt_groups) X(rt_rows) X(part_search) X(enc_part_search) X(auto_nbuf)
 #define PMRC_COUNT(m) +1
-static_assert(0 PMRC_GEN_FIELDS(PMRC_COUNT) == 42 && sizeof(GenOptions) == 140,
+static_assert(0 PMRC_GEN_FIELDS(PMRC_COUNT) == 43 && sizeof(GenOptions) == 144,
               "GenOptions changed: list every field in PMRC_GEN_FIELDS (the plan index key)");
 #undef PMRC_COUNT
 
@@ -294,6 +294,19 @@ static GenOptions resolve_options(const PlanSpec &p, const GenOptions &o) {
     oo.team = std::max(1, oo.ws_prod) + 2;
     oo.warps = oo.team * std::min(4, 12 / oo.team);
     oo.nbuf = 2;
+  }
+  // A 3-deep stage ring when it still fits 16 warps (stages of <= 9 blocks: the k = 4 codes):
+  // these plans are HBM-bound and latency-limited, and prefetching two items ahead lifts the MSR
+  // k = 4 encode from 0.391 to 0.366 ms (0.84 -> 0.90 of HBM; 24 warps: 0.362, but they cost MBR
+  // k = 4 30%); MBR k = 4 is unchanged (0.459 / 0.458) (profiles/r02/k4_knobs.jsonl)
+  if (o.auto_nbuf && oo.nbuf == 2 && oo.layout >= 1 && !oo.ws && p.w != 16 && (oo.warps <= 0 || oo.warps == 16)) {
+    GenOptions o3 = oo;
+    o3.nbuf = 3;
+    GenStats p3;
+    probe(p, o3, p3);
+    const int budget3 = o.smem_kib > 0 ? o.smem_kib * 1024 : 225 * 1024;
+    // (plans of several groups only: the one-group RS encode measured 0.337 -> 0.360 ms with it)
+    if (p3.groups > 1 && p3.smem_per_warp > 0 && budget3 / p3.smem_per_warp >= 16) oo.nbuf = 3;
   }
   // warps per CTA from the shared-memory budget (2 stage buffers of in_block KiB per team)
   GenStats pr;

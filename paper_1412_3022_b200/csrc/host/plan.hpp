@@ -92,6 +92,7 @@ struct GenOptions {
   int rt_rows = 0;          // runtime-coefficient kernel: rows per thread, 7 or 8 (0 = auto)
   int part_search = 0;      // evaluations of the input / row partition search per single-stage group (codegen.cpp)
   int enc_part_search = 200; // part_search of the encode plan (built once per code; capi.cpp)
+  bool auto_nbuf = true;    // resolve_options: a 3-deep stage ring for multi-group plans when it still fits 16 warps (k = 4 codes)
 };
 
 constexpr int kDynSlots = 64;  // counter slots of the dynamic schedule (launches in flight per plan)
